@@ -1,0 +1,225 @@
+/*
+ * include/msk.h -- C-ABI of libmsk, the B200-native (sm_100a, FP64) hot path
+ * of Lot & Rieger's monolithic kernel-based multiscale method
+ * (arXiv 2503.04914; /root/reference/PAPER.md cited as P:<line>).
+ *
+ * The problem: reconstruct f : Omega in R^d
+ * -> R from samples f^{(l)} = f|_{X_l} on a hierarchy X_1, ..., X_L with
+ * per-level support radii delta_l and a Wendland function phi_{d,k}.  The
+ * coefficients alpha^{(l)} solve the block-lower-triangular system
+ * T_L alpha = f (eq:bigt), i.e. for l = 1..L
+ *     A_l alpha^{(l)} = f^{(l)} - sum_{k<l} B_{lk} alpha^{(k)}      (eq:mas P:287)
+ * with A_l = (Phi_{delta_l}(x_i^{(l)} - x_j^{(l)})),
+ *      B_{lk} = (Phi_{delta_k}(x_i^{(l)} - x_j^{(k)}))  (column level's delta,
+ *      P:276, reading C-1),
+ *      Phi_delta(x) = delta^{-d} phi_{d,k}(||x||_2 / delta)   (eq:kernelscaling P:67).
+ * The library solves it as the paper does, through the split
+ * D_L alpha = beta, T'_L beta = f (eq:split P:585-591): an L-sweep Jacobi
+ * iteration on T'_L (Theorem jacobi, Algorithm 2) and
+ * block-diagonal conjugate gradients on the SPD A_l (Theorem cg P:603-661,
+ * Algorithm 1).  The approximant is
+ *     f_L(x) = sum_l sum_n alpha_n^{(l)} Phi_{delta_l}(x - x_n^{(l)})  (eq:fapproximation P:295).
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ * - Every pointer to bulk data (points, f, alpha, x, s, v, y) may be HOST or
+ *   DEVICE memory (on the context's device); the library detects which with
+ *   cudaPointerGetAttributes and copies host data through its own stream.
+ *   Small parameter arrays marked [host] must be host memory.
+ * - Points are row-major n x d FP64 ("x-major": x, y[, z] of point 0, then
+ *   point 1, ...).  Vectors are FP64 in the CALLER's point order.
+ * - All calls are synchronous with respect to the host: on return every
+ *   output is written and the context stream is idle.
+ * - The caller owns every buffer it passes; the library deep-copies inputs
+ *   it keeps (points, delta, q).  Handles are opaque, not thread-safe, and
+ *   destroyed explicitly.  Distinct handles are independent.
+ * - Every call returns an msk_status.  No C++ exception crosses the ABI.
+ *   On error the outputs are unspecified and msk_last_error() (thread-local,
+ *   valid until the next call on the same thread) names the cause.
+ * - There is no CPU fallback: if no CUDA device is usable every call that
+ *   needs one fails with MSK_ERR_CUDA.
+ */
+#ifndef MSK_H
+#define MSK_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MSK_API __attribute__((visibility("default")))
+#else
+#define MSK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MSK_OK = 0,
+    MSK_ERR_INVALID = 1,  /* bad argument: d not in {2,3}; L<1 or L>16; n[l]<1; delta<=0 or
+                             non-finite; k not in {0,1,2}; duplicate points in a level
+                             (q_l = 0 => A_l singular); tol not in (0,1); null pointer */
+    MSK_ERR_NOMEM = 2,    /* device allocation failed */
+    MSK_ERR_CUDA = 3,     /* CUDA runtime error (includes: no device) */
+    MSK_ERR_NCCL = 4,     /* reserved for the multi-GPU communicator */
+    MSK_ERR_NOCONV = 5,   /* CG reached max_iter; msk_last_error names level and residual */
+    MSK_ERR_STATE = 6     /* call out of order (e.g. msk_solve before msk_assemble) */
+} msk_status;
+
+/* msk_hierarchy_create flags */
+#define MSK_FLAG_NONE 0u
+
+/* msk_solve schedules */
+#define MSK_SCHED_PRUNED 0u  /* Algorithm 2 with each inner solve t^{(l)} = A_l^{-1} beta^{(l)} done
+                                once, when beta^{(l)} is final; beta bit-identical to LITERAL */
+#define MSK_SCHED_LITERAL 1u /* Algorithm 2 as printed: L sweeps x (L-1) inner solves, then the
+                                block-diagonal CG on all levels */
+
+#define MSK_MAX_LEVELS 16
+
+typedef struct msk_ctx msk_ctx;
+typedef struct msk_hierarchy msk_hierarchy;
+
+/* Per-solve report (msk_solve, nullable). */
+typedef struct {
+    int32_t L;
+    int32_t jacobi_sweeps;                  /* L for LITERAL; 0 for PRUNED (lazy sweeps)        */
+    int32_t cg_iters[MSK_MAX_LEVELS];       /* iterations of the solve that produced alpha_l    */
+    int32_t inner_iters[MSK_MAX_LEVELS];    /* sum of inner Jacobi CG iterations per level      */
+    double rel_res[MSK_MAX_LEVELS];         /* final recurrence ||r||/||b|| per level           */
+    double nnz_cg;                          /* Wendland nonzeros read by CG SpMVs               */
+    double nnz_gather;                      /* Wendland nonzeros evaluated by the B products    */
+    double bytes_cg;                        /* algorithmic HBM bytes of the CG launches         */
+    double t_cg_ms;                         /* device time of the CG launches (CUDA events)     */
+    double t_gather_ms;                     /* device time of the B-product launches            */
+    double t_total_ms;                      /* device time of the whole call                    */
+    double t_cg_level_ms[MSK_MAX_LEVELS];   /* device time of the CG launch(es) per level       */
+    double bytes_cg_level[MSK_MAX_LEVELS];  /* algorithmic bytes of those launches              */
+    int32_t launches;                       /* kernels launched by the call                     */
+} msk_solve_info;
+
+/* Per-hierarchy facts (msk_hierarchy_info). */
+typedef struct {
+    int32_t d, L, k;
+    int64_t n[MSK_MAX_LEVELS];
+    int64_t nnz_A[MSK_MAX_LEVELS];          /* nnz of assembled A_l (0 before msk_assemble)     */
+    int64_t ncells[MSK_MAX_LEVELS];         /* cells of level l's uniform grid                  */
+    double delta[MSK_MAX_LEVELS];
+    double q[MSK_MAX_LEVELS];               /* given, or 1/2 min pair distance        */
+    double t_create_ms, t_assemble_ms;      /* device time of the last create / assemble        */
+    int32_t launches_create, launches_assemble;
+} msk_hierarchy_info;
+
+/* Per-evaluation report (msk_evaluate_ex, nullable). */
+typedef struct {
+    double nnz;                             /* Wendland nonzeros evaluated                      */
+    double t_sort_ms, t_eval_ms, t_total_ms;
+    int32_t launches;
+} msk_eval_info;
+
+/* ---------------------------------------------------------------- context */
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t of
+ * that device to enqueue on, or NULL to let the library create its own.
+ * rank / world_size / nccl_unique_id: reserved for the partitioned
+ * multi-GPU path; this version requires world_size == 1 (rank 0,
+ * nccl_unique_id NULL) and returns MSK_ERR_INVALID otherwise. */
+MSK_API msk_status msk_ctx_create(int device, void *cuda_stream, int rank, int world_size,
+                          const void *nccl_unique_id, msk_ctx **out);
+MSK_API void msk_ctx_destroy(msk_ctx *ctx);
+
+/* ------------------------------------------------------------- hierarchy */
+
+/* a0 + a1: ingest the hierarchy X_1..X_L (Assumption pointset P:87-114) and
+ * build one uniform-grid cell list per level (cell side >= delta_l; points
+ * stably sorted by (cell key, original index)).
+ *   d            2 or 3.
+ *   L            1..16 levels, coarse to fine.
+ *   n [host]     L point counts.
+ *   points       L pointers, each n[l] x d row-major FP64 (host or device).
+ *   delta [host] L support radii delta_l > 0 (eq:deltadef P:105-107: nu h_l).
+ *   q [host]     L separation values (used only by thresholding), or
+ *                NULL: computed exactly as 1/2 min distance when the
+ *                closest pair lies within delta_l, else reported as delta_l/2.
+ *   wendland_k   0, 1 or 2: phi_{d,k} (reading C-3).
+ *   flags        MSK_FLAG_NONE.
+ * Duplicate points within one level => MSK_ERR_INVALID. */
+MSK_API msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int64_t *n,
+                                const double *const *points, const double *delta,
+                                const double *q, int wendland_k, uint32_t flags,
+                                msk_hierarchy **out);
+MSK_API void msk_hierarchy_destroy(msk_hierarchy *h);
+
+/* Facts about the hierarchy (sizes, nnz, timings of the last create/assemble). */
+MSK_API msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_info *info);
+
+/* a2 (+ a6 later): assemble the level matrices A_l in CSR (pattern r^2 <
+ * delta_l^2, strict, bit-exact; values Phi_{delta_l}).  T <= 0: exact mode
+ * (B_{kl} stay matrix-free).  T > 0 (thresholded factor M~(T), eq:
+ * perturbedmatrix P:846-861) is not available in this version and returns
+ * MSK_ERR_INVALID.  lagrange_tol is reserved for T > 0. */
+MSK_API msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol);
+
+/* a3-a5, a8: solve T_L alpha = f (eq:bigt) through eq:split.
+ *   f      L pointers to f^{(l)} (n[l] FP64, caller order, host or device).
+ *   tol    relative CG tolerance in (0,1): stop when ||r||_2 <= tol ||b||_2
+ *          per level (reading C-9); inner Jacobi solves use tol/10 (C-10).
+ *   max_iter  CG iteration cap per solve (>= 1).
+ *   schedule  MSK_SCHED_PRUNED or MSK_SCHED_LITERAL.
+ *   alpha  L pointers to caller-owned outputs alpha^{(l)} (n[l] FP64, caller
+ *          order, host or device).
+ *   info   nullable report.
+ * Requires msk_assemble.  A zero right-hand side gives alpha = 0 after 0
+ * iterations.  Non-convergence => MSK_ERR_NOCONV ("level l: rel. residual r
+ * after k iterations"). */
+MSK_API msk_status msk_solve(msk_hierarchy *h, const double *const *f, double tol, int32_t max_iter,
+                     uint32_t schedule, double *const *alpha, msk_solve_info *info);
+
+/* a9: s_j = f_L(x_j) = sum_l sum_n alpha_n^{(l)} Phi_{delta_l}(x_j - x_n^{(l)})
+ * (eq:fapproximation P:293-296) for m points x (m x d row-major, host or
+ * device), using the alpha of the last successful msk_solve.  s: m FP64
+ * (host or device).  m = 0 is allowed.  MSK_ERR_STATE before msk_solve. */
+MSK_API msk_status msk_evaluate(msk_hierarchy *h, int64_t m, const double *x, double *s);
+MSK_API msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x, double *s,
+                           msk_eval_info *info);
+
+/* ----------------------------------------- row-level entry points (tests) */
+
+/* Sparsity pattern (and optionally values) of block B_{row_level,col_level}
+ * (row_level >= col_level; row_level == col_level gives A_l), in CALLER
+ * indices with ascending columns.  row_ptr [host]: n[row_level]+1 int64,
+ * always written.  col [host] / val [host]: nnz entries, or NULL to query
+ * nnz (= row_ptr[n]) first.  0-based levels.  Pattern r^2 < delta_col^2 is
+ * bit-exact (reading C-4). */
+MSK_API msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_level, int64_t *row_ptr,
+                            int32_t *col, double *val);
+
+/* Cell list of level l [host outputs]: perm (n[l] int32, sorted position ->
+ * caller index), cell_start (ncells+1 int32), cell_key (n[l] int64, key of
+ * each sorted point), origin lo (d doubles), cell side, grid dims (d int64).
+ * Any output may be NULL. */
+MSK_API msk_status msk_export_cells(msk_hierarchy *h, int level, int32_t *perm, int32_t *cell_start,
+                            int64_t *cell_key, double *lo, double *cell, int64_t *dims);
+
+/* y = B_{row_level,col_level} v (a3).  row_level == col_level uses the
+ * assembled A_l (CSR SpMV kernel; requires msk_assemble), row_level >
+ * col_level the matrix-free kernel.  v: n[col_level], y: n[row_level], caller
+ * order, host or device.  t_ms (nullable): device time of the kernel launch. */
+MSK_API msk_status msk_apply_block(msk_hierarchy *h, int row_level, int col_level, const double *v,
+                           double *y, double *t_ms);
+
+/* a4 on one level: x = A_l^{-1} b by the library's CG (x0 = 0), caller order,
+ * host or device.  iters / rel_res / t_ms nullable. */
+MSK_API msk_status msk_cg_level(msk_hierarchy *h, int level, const double *b, double *x, double tol,
+                        int32_t max_iter, int32_t *iters, double *rel_res, double *t_ms);
+
+/* Thread-local description of the last error ("" if none). */
+MSK_API const char *msk_last_error(void);
+
+/* Library version string. */
+MSK_API const char *msk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSK_H */

@@ -187,7 +187,7 @@ def _hier_args(points, delta):
     return pts, d, n, _c(delta)
 
 
-def sequential(points, delta, f, tol=1e-12, k=1, max_iter=20000, direct_max_n=4000):
+def sequential(points, delta, f, tol=1e-12, k=1, max_iter=20000, direct_max_n=4000, count=True):
     """eq:mas level by level (O4). Returns (alpha list, iters list, counters)."""
     pts, d, n, dl = _hier_args(points, delta)
     fs = [_c(x) for x in f]
@@ -198,7 +198,8 @@ def sequential(points, delta, f, tol=1e-12, k=1, max_iter=20000, direct_max_n=40
     fp, _k2 = _ptrs(fs)
     ap, _k3 = _ptrs(alpha)
     st = lib().mo_sequential(d, k, len(pts), _ptr(n, _i64p), pp, _ptr(dl), fp, float(tol),
-                             int(max_iter), int(direct_max_n), ap, iters, _ptr(counters))
+                             int(max_iter), int(direct_max_n), ap, iters,
+                             _ptr(counters) if count else None)
     if st:
         raise RuntimeError(f"oracle sequential solve failed ({st})")
     return alpha, list(iters), counters

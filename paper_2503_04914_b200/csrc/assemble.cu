@@ -1,0 +1,104 @@
+// assemble.cu -- a2: CSR pattern and values of A_l (and of B_{kl} blocks for
+// export).  Pattern: r^2 < delta^2 with r^2 evaluated left to right without
+// FMA and delta^2 computed once on the host (reading C-4) -- bit-exact with
+// the definition.  Values Phi_delta(r) = delta^-d phi(r / delta)
+// (eq:kernelscaling P:67) with the column level's delta (reading C-1).
+#include "kernels.cuh"
+#include "neighbors.cuh"
+
+namespace msk {
+
+namespace {
+constexpr int NT = 256;
+
+template <int D>
+__global__ void __launch_bounds__(NT) k_count(LevelView rows, LevelView cols, int same,
+                                              int32_t *__restrict__ cnt,
+                                              unsigned long long *__restrict__ min_r2_bits) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    if (i < rows.n) {
+        double x[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = rows.x[a][i];
+        int c = 0;
+        const double d2 = cols.delta2;
+        for_each_range<D>(cols, x, [&](int b, int e) {
+            for (int j = b; j < e; ++j) {
+                double y[3];
+#pragma unroll
+                for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
+                double r2 = dist2_nofma<D>(x, y);
+                if (r2 < d2) {
+                    ++c;
+                    if (same && j != i && r2 < best) best = r2;
+                }
+            }
+        });
+        cnt[i] = c;
+    }
+    if (min_r2_bits) {
+        // block min of non-negative doubles via their ordered bit patterns
+        unsigned long long bits = (unsigned long long)__double_as_longlong(best);
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long t = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = t < bits ? t : bits;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMin(min_r2_bits, bits);
+    }
+}
+
+template <int D, int K>
+__global__ void __launch_bounds__(NT) k_fill(LevelView rows, LevelView cols,
+                                             const int64_t *__restrict__ row_ptr,
+                                             int32_t *__restrict__ col, double *__restrict__ val) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (i >= rows.n) return;
+    double x[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = rows.x[a][i];
+    int64_t p = row_ptr[i];
+    const double d2 = cols.delta2, inv = cols.inv_delta, sc = cols.scale;
+    for_each_range<D>(cols, x, [&](int b, int e) {
+        for (int j = b; j < e; ++j) {
+            double y[3];
+#pragma unroll
+            for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
+            double r2 = dist2_nofma<D>(x, y);
+            if (r2 < d2) {
+                col[p] = j;
+                if (val) val[p] = sc * wendland<K>(sqrt(r2) * inv);
+                ++p;
+            }
+        }
+    });
+}
+}  // namespace
+
+void count_pattern(int d, const LevelView &rows, const LevelView &cols, bool same, int32_t *cnt,
+                   unsigned long long *min_r2_bits, cudaStream_t st, int *launches) {
+    if (rows.n == 0) return;
+    unsigned nb = ceil_div_u(rows.n, NT);
+    if (d == 2) k_count<2><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits);
+    else k_count<3><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits);
+    MSK_CHECK_LAUNCH();
+    if (launches) *launches += 1;
+}
+
+void fill_pattern(int d, int k, const LevelView &rows, const LevelView &cols,
+                  const int64_t *row_ptr, int32_t *col, double *val, cudaStream_t st,
+                  int *launches) {
+    if (rows.n == 0) return;
+    unsigned nb = ceil_div_u(rows.n, NT);
+#define MSK_FILL(DD, KK) k_fill<DD, KK><<<nb, NT, 0, st>>>(rows, cols, row_ptr, col, val)
+    if (d == 2) {
+        if (k == 0) MSK_FILL(2, 0); else if (k == 1) MSK_FILL(2, 1); else MSK_FILL(2, 2);
+    } else {
+        if (k == 0) MSK_FILL(3, 0); else if (k == 1) MSK_FILL(3, 1); else MSK_FILL(3, 2);
+    }
+#undef MSK_FILL
+    MSK_CHECK_LAUNCH();
+    if (launches) *launches += 1;
+}
+
+}  // namespace msk

@@ -1,0 +1,910 @@
+// capi.cu -- the C-ABI of libmsk (include/msk.h): argument checking, device
+// memory (stream-ordered pool), host/device pointer handling, and the
+// orchestration of the hot-path kernels:
+//   create   : a0 ingest + a1 cell lists + pattern row counts (q, duplicates)
+//   assemble : a2 CSR of A_l
+//   solve    : a5 Jacobi (pruned or literal schedule) + a4/a8 block CG
+//   evaluate : a9
+// Every step of the path runs in the kernels of this library; there is no
+// host compute path and no CPU fallback.
+#include <math.h>
+#include <stdio.h>
+
+#include <cmath>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/msk.h"
+#include "kernels.cuh"
+
+using namespace msk;
+
+// ------------------------------------------------------------------ state
+struct msk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+};
+
+namespace {
+
+struct LevelData {
+    int64_t n = 0;
+    double delta = 0, q = 0;
+    Grid g{};
+    double *xs = nullptr;          // d * n SoA, spatial order
+    int32_t *perm = nullptr;       // spatial -> caller
+    int32_t *cell_start = nullptr; // ncells + 1
+    int32_t *cnt = nullptr;        // A_l row counts (spatial order)
+    int64_t nnz = 0;
+    int64_t *row_ptr = nullptr;
+    int32_t *col = nullptr;
+    double *val = nullptr;
+    double *alpha = nullptr;       // coefficients of the last solve, spatial order
+};
+
+thread_local std::string g_err;
+
+void set_err(const std::string &s) { g_err = s; }
+
+template <typename T>
+T *dalloc(size_t count, cudaStream_t st) {
+    T *p = nullptr;
+    if (count == 0) count = 1;
+    MSK_CUDA(cudaMallocAsync((void **)&p, sizeof(T) * count, st));
+    return p;
+}
+
+void dfree(void *p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// A device view of a caller buffer: the buffer itself if it is device memory,
+// else a stream-ordered device copy.
+struct DevBuf {
+    const double *ptr = nullptr;
+    double *owned = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf() = default;
+    DevBuf(const double *p, size_t count, cudaStream_t s) : st(s) {
+        if (is_device_ptr(p)) {
+            ptr = p;
+        } else {
+            owned = dalloc<double>(count, s);
+            if (count) MSK_CUDA(cudaMemcpyAsync(owned, p, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+            ptr = owned;
+        }
+    }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), owned(o.owned), st(o.st) { o.owned = nullptr; }
+    ~DevBuf() { dfree(owned, st); }
+};
+
+// A device output for a caller buffer; flush() copies back when it is host memory.
+struct DevOut {
+    double *ptr = nullptr;
+    double *host = nullptr;
+    size_t count = 0;
+    cudaStream_t st = nullptr;
+    DevOut() = default;
+    DevOut(double *p, size_t c, cudaStream_t s) : count(c), st(s) {
+        if (is_device_ptr(p)) {
+            ptr = p;
+        } else {
+            host = p;
+            ptr = dalloc<double>(c, s);
+        }
+    }
+    DevOut(const DevOut &) = delete;
+    DevOut &operator=(const DevOut &) = delete;
+    DevOut(DevOut &&o) noexcept : ptr(o.ptr), host(o.host), count(o.count), st(o.st) { o.host = nullptr; }
+    void flush() {
+        if (host && count)
+            MSK_CUDA(cudaMemcpyAsync(host, ptr, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    }
+    ~DevOut() {
+        if (host) dfree(ptr, st);
+    }
+};
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t st;
+    explicit Timer(cudaStream_t s) : st(s) {
+        MSK_CUDA(cudaEventCreate(&a));
+        MSK_CUDA(cudaEventCreate(&b));
+    }
+    void start() { MSK_CUDA(cudaEventRecord(a, st)); }
+    void stop() { MSK_CUDA(cudaEventRecord(b, st)); }
+    double ms() {  // after a stream synchronisation
+        float t = 0;
+        MSK_CUDA(cudaEventElapsedTime(&t, a, b));
+        return t;
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+#define API_BEGIN try {
+#define API_END                                                  \
+    return MSK_OK;                                               \
+    }                                                            \
+    catch (const msk::Error &e) {                                \
+        set_err(e.what());                                       \
+        return (msk_status)e.status;                             \
+    }                                                            \
+    catch (const std::bad_alloc &) {                             \
+        set_err("host allocation failed");                       \
+        return MSK_ERR_NOMEM;                                    \
+    }                                                            \
+    catch (const std::exception &e) {                            \
+        set_err(e.what());                                       \
+        return MSK_ERR_CUDA;                                     \
+    }
+
+void require(bool ok, const std::string &msg) {
+    if (!ok) throw Error(MSK_ERR_INVALID, msg);
+}
+
+}  // namespace
+
+struct msk_hierarchy {
+    msk_ctx *ctx = nullptr;
+    int d = 0, L = 0, k = 0;
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    LevelData lev[kMaxLevels];
+    bool assembled = false, solved = false;
+    int64_t ntot = 0;
+    int64_t off[kMaxLevels + 1] = {0};
+    double *ws = nullptr;  // CG workspace: r, p, q, beta, t (5 * ntot)
+    double t_create_ms = 0, t_assemble_ms = 0;
+    int launches_create = 0, launches_assemble = 0;
+
+    cudaStream_t st() const { return ctx->stream; }
+
+    LevelView view(int l, const double *coef = nullptr) const {
+        const LevelData &D = lev[l];
+        LevelView v{};
+        v.n = D.n;
+        for (int a = 0; a < 3; ++a) v.x[a] = a < d ? D.xs + (size_t)a * D.n : nullptr;
+        v.cell_start = D.cell_start;
+        v.g = D.g;
+        v.delta2 = D.delta * D.delta;
+        v.inv_delta = 1.0 / D.delta;
+        v.scale = pow(D.delta, -(double)d);
+        v.coef = coef;
+        return v;
+    }
+
+    void ensure_ws() {
+        if (!ws) ws = dalloc<double>((size_t)(5 * ntot), st());
+    }
+    double *ws_r(int l) { return ws + off[l]; }
+    double *ws_p(int l) { return ws + ntot + off[l]; }
+    double *ws_q(int l) { return ws + 2 * ntot + off[l]; }
+    double *ws_beta(int l) { return ws + 3 * ntot + off[l]; }
+    double *ws_t(int l) { return ws + 4 * ntot + off[l]; }
+
+    void release() {
+        cudaStream_t s = st();
+        for (int l = 0; l < L; ++l) {
+            LevelData &D = lev[l];
+            dfree(D.xs, s); dfree(D.perm, s); dfree(D.cell_start, s); dfree(D.cnt, s);
+            dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s);
+            D = LevelData();
+        }
+        dfree(ws, s);
+        ws = nullptr;
+    }
+};
+
+// ================================================================= context
+extern "C" msk_status msk_ctx_create(int device, void *cuda_stream, int rank, int world_size,
+                                     const void *nccl_unique_id, msk_ctx **out) {
+    API_BEGIN
+    require(out != nullptr, "msk_ctx_create: out is NULL");
+    *out = nullptr;
+    require(world_size == 1 && rank == 0 && nccl_unique_id == nullptr,
+            "msk_ctx_create: only world_size == 1 is supported by this version");
+    int ndev = 0;
+    MSK_CUDA(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, "msk_ctx_create: bad device index");
+    MSK_CUDA(cudaSetDevice(device));
+    msk_ctx *c = new msk_ctx();
+    c->device = device;
+    if (cuda_stream) {
+        c->stream = (cudaStream_t)cuda_stream;
+    } else {
+        MSK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    // keep freed blocks in the stream-ordered pool: repeated create/solve
+    // cycles then allocate without device-wide synchronisation
+    cudaMemPool_t pool;
+    MSK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ull;
+    MSK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    cg_max_resident_blocks();
+    *out = c;
+    API_END
+}
+
+extern "C" void msk_ctx_destroy(msk_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+// =============================================================== hierarchy
+extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int64_t *n,
+                                           const double *const *points, const double *delta,
+                                           const double *q, int wendland_k, uint32_t flags,
+                                           msk_hierarchy **out) {
+    msk_hierarchy *h = nullptr;
+    try {
+        require(ctx && out && n && points && delta, "msk_hierarchy_create: NULL argument");
+        *out = nullptr;
+        require(d == 2 || d == 3, "msk_hierarchy_create: d must be 2 or 3");
+        require(L >= 1 && L <= kMaxLevels, "msk_hierarchy_create: L must be in 1..16");
+        require(wendland_k >= 0 && wendland_k <= 2, "msk_hierarchy_create: k must be 0, 1 or 2");
+        require(flags == MSK_FLAG_NONE, "msk_hierarchy_create: unknown flags");
+        for (int l = 0; l < L; ++l) {
+            require(n[l] >= 1 && n[l] < (1ll << 31) - 1, "msk_hierarchy_create: n[l] out of range");
+            require(points[l] != nullptr, "msk_hierarchy_create: NULL points");
+            require(std::isfinite(delta[l]) && delta[l] > 0, "msk_hierarchy_create: delta must be finite and > 0");
+            if (q) require(std::isfinite(q[l]) && q[l] > 0, "msk_hierarchy_create: q must be finite and > 0");
+        }
+        MSK_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        h = new msk_hierarchy();
+        h->ctx = ctx;
+        h->d = d;
+        h->L = L;
+        h->k = wendland_k;
+        Timer tm(st);
+        tm.start();
+        int launches = 0;
+        // ---- a0: ingest (device copies of host inputs) + bounding box
+        std::vector<DevBuf> pts;
+        pts.reserve(L);
+        unsigned long long *mm = dalloc<unsigned long long>(6, st);
+        unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+        MSK_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+        for (int l = 0; l < L; ++l) {
+            pts.emplace_back(points[l], (size_t)(n[l] * d), st);
+            minmax_points(n[l], d, pts.back().ptr, mm, st, &launches);
+        }
+        unsigned long long mmh[6];
+        MSK_CUDA(cudaMemcpyAsync(mmh, mm, sizeof mmh, cudaMemcpyDeviceToHost, st));
+        MSK_CUDA(cudaStreamSynchronize(st));
+        dfree(mm, st);
+        for (int a = 0; a < d; ++a) {
+            h->lo[a] = ord_key_to_double(mmh[a]);
+            h->hi[a] = ord_key_to_double(mmh[3 + a]);
+            require(std::isfinite(h->lo[a]) && std::isfinite(h->hi[a]),
+                    "msk_hierarchy_create: non-finite point coordinates");
+        }
+        // ---- a1: per-level uniform grid + cell list; pattern row counts
+        std::vector<unsigned long long *> minr2(L);
+        for (int l = 0; l < L; ++l) {
+            LevelData &D = h->lev[l];
+            D.n = n[l];
+            D.delta = delta[l];
+            h->off[l + 1] = h->off[l] + n[l];
+            double cell = delta[l] * (1.0 + 0x1p-20);
+            for (;;) {
+                Grid g{};
+                g.inv_cell = 1.0 / cell;
+                g.ncells = 1;
+                for (int a = 0; a < 3; ++a) {
+                    g.lo[a] = a < d ? h->lo[a] : 0.0;
+                    g.dim[a] = a < d ? (int64_t)floor((h->hi[a] - h->lo[a]) * g.inv_cell) + 1 : 1;
+                    g.ncells *= g.dim[a];
+                }
+                // bound the cell count (points much sparser than delta): larger
+                // cells only add candidates, never lose neighbours
+                if (g.ncells <= 8 * n[l] + 4096) {
+                    D.g = g;
+                    break;
+                }
+                cell *= 1.5;
+            }
+            D.xs = dalloc<double>((size_t)(d * n[l]), st);
+            D.perm = dalloc<int32_t>((size_t)n[l], st);
+            D.cell_start = dalloc<int32_t>((size_t)(D.g.ncells + 1), st);
+            CellListOut co{};
+            co.perm = D.perm;
+            for (int a = 0; a < d; ++a) co.xs[a] = D.xs + (size_t)a * n[l];
+            co.cell_start = D.cell_start;
+            co.keys = nullptr;
+            build_cell_list(d, n[l], pts[l].ptr, D.g, true, co, st, &launches);
+            D.cnt = dalloc<int32_t>((size_t)n[l], st);
+            minr2[l] = dalloc<unsigned long long>(1, st);
+            unsigned long long inf = 0x7ff0000000000000ull;
+            MSK_CUDA(cudaMemcpyAsync(minr2[l], &inf, sizeof inf, cudaMemcpyHostToDevice, st));
+            LevelView v = h->view(l);
+            count_pattern(d, v, v, true, D.cnt, minr2[l], st, &launches);
+        }
+        h->ntot = h->off[L];
+        std::vector<unsigned long long> mr(L);
+        for (int l = 0; l < L; ++l)
+            MSK_CUDA(cudaMemcpyAsync(&mr[l], minr2[l], sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        tm.stop();
+        MSK_CUDA(cudaStreamSynchronize(st));
+        for (int l = 0; l < L; ++l) {
+            dfree(minr2[l], st);
+            double r2;
+            memcpy(&r2, &mr[l], sizeof r2);
+            require(r2 > 0.0, "msk_hierarchy_create: duplicate points in level " + std::to_string(l));
+            h->lev[l].q = q ? q[l] : (std::isfinite(r2) ? 0.5 * sqrt(r2) : 0.5 * delta[l]);
+        }
+        h->t_create_ms = tm.ms();
+        h->launches_create = launches;
+        *out = h;
+        return MSK_OK;
+    } catch (const msk::Error &e) {
+        set_err(e.what());
+        if (h) { h->release(); delete h; }
+        return (msk_status)e.status;
+    } catch (const std::exception &e) {
+        set_err(e.what());
+        if (h) { h->release(); delete h; }
+        return MSK_ERR_CUDA;
+    }
+}
+
+extern "C" void msk_hierarchy_destroy(msk_hierarchy *h) {
+    if (!h) return;
+    cudaSetDevice(h->ctx->device);
+    h->release();
+    cudaStreamSynchronize(h->st());
+    delete h;
+}
+
+extern "C" msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_info *info) {
+    API_BEGIN
+    require(h && info, "msk_hierarchy_info_get: NULL argument");
+    memset(info, 0, sizeof *info);
+    info->d = h->d;
+    info->L = h->L;
+    info->k = h->k;
+    for (int l = 0; l < h->L; ++l) {
+        info->n[l] = h->lev[l].n;
+        info->nnz_A[l] = h->lev[l].nnz;
+        info->ncells[l] = h->lev[l].g.ncells;
+        info->delta[l] = h->lev[l].delta;
+        info->q[l] = h->lev[l].q;
+    }
+    info->t_create_ms = h->t_create_ms;
+    info->t_assemble_ms = h->t_assemble_ms;
+    info->launches_create = h->launches_create;
+    info->launches_assemble = h->launches_assemble;
+    API_END
+}
+
+// ================================================================ assemble
+extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol) {
+    API_BEGIN
+    require(h != nullptr, "msk_assemble: NULL hierarchy");
+    require(!(T > 0.0), "msk_assemble: the thresholded factor (T > 0) is not available in this version");
+    (void)lagrange_tol;
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    Timer tm(st);
+    tm.start();
+    int launches = 0;
+    std::vector<int64_t> nnz(h->L);
+    for (int l = 0; l < h->L; ++l) {
+        LevelData &D = h->lev[l];
+        dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st);
+        D.row_ptr = dalloc<int64_t>((size_t)(D.n + 1), st);
+        exclusive_scan_i64(D.cnt, D.n, D.row_ptr, st, &launches);
+        MSK_CUDA(cudaMemcpyAsync(&nnz[l], D.row_ptr + D.n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
+    MSK_CUDA(cudaStreamSynchronize(st));
+    for (int l = 0; l < h->L; ++l) {
+        LevelData &D = h->lev[l];
+        D.nnz = nnz[l];
+        D.col = dalloc<int32_t>((size_t)D.nnz, st);
+        D.val = dalloc<double>((size_t)D.nnz, st);
+        LevelView v = h->view(l);
+        fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
+    }
+    tm.stop();
+    MSK_CUDA(cudaStreamSynchronize(st));
+    h->t_assemble_ms = tm.ms();
+    h->launches_assemble = launches;
+    h->assembled = true;
+    API_END
+}
+
+// =================================================================== solve
+namespace {
+
+struct LevelStat {
+    int iters, status;
+    double rr, bb;
+};
+
+// one CG launch over the given levels; returns per-level stats (host) after sync
+CGLevelArgs cg_args(msk_hierarchy *h, int l, double tol, int max_iter, const double *b,
+                    const double *b_src, double *x, double *x_out, int *d_iters, double *d_rr,
+                    int *d_status) {
+    LevelData &D = h->lev[l];
+    CGLevelArgs a{};
+    a.n = D.n;
+    a.nnz = D.nnz;
+    a.row_ptr = D.row_ptr;
+    a.col = D.col;
+    a.val = D.val;
+    a.b = b;
+    a.b_src = b_src;
+    a.b_perm = b_src ? D.perm : nullptr;
+    a.x = x;
+    a.r = h->ws_r(l);
+    a.p = h->ws_p(l);
+    a.q = h->ws_q(l);
+    a.x_out = x_out;
+    a.x_perm = x_out ? D.perm : nullptr;
+    a.tol2 = tol * tol;
+    a.max_iter = max_iter;
+    a.nblocks = 0;
+    a.out_iters = d_iters;
+    a.out_rr = d_rr;
+    a.out_status = d_status;
+    return a;
+}
+
+double cg_bytes(const LevelData &D, int iters) {
+    // algorithmic bytes: per iteration 12 B/nnz (val + col)
+    // + 96 B/row (row_ptr 8, gathered p 8, q 8, x/r/p/q updates 72); init 32 B/row
+    return (double)iters * (12.0 * (double)D.nnz + 96.0 * (double)D.n) + 32.0 * (double)D.n;
+}
+
+}  // namespace
+
+extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double tol,
+                                int32_t max_iter, uint32_t schedule, double *const *alpha,
+                                msk_solve_info *info) {
+    API_BEGIN
+    require(h && f && alpha, "msk_solve: NULL argument");
+    require(tol > 0.0 && tol < 1.0, "msk_solve: tol must be in (0,1)");
+    require(max_iter >= 1, "msk_solve: max_iter must be >= 1");
+    require(schedule == MSK_SCHED_PRUNED || schedule == MSK_SCHED_LITERAL, "msk_solve: unknown schedule");
+    if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_solve: call msk_assemble first");
+    for (int l = 0; l < h->L; ++l) require(f[l] && alpha[l], "msk_solve: NULL level pointer");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const int L = h->L;
+    const double inner_tol = tol / 10.0;  // reading C-10
+    h->ensure_ws();
+    for (int l = 0; l < L; ++l)
+        if (!h->lev[l].alpha) h->lev[l].alpha = dalloc<double>((size_t)h->lev[l].n, st);
+
+    std::vector<DevBuf> fd;
+    std::vector<DevOut> ad;
+    fd.reserve(L);
+    ad.reserve(L);
+    for (int l = 0; l < L; ++l) {
+        fd.emplace_back(f[l], (size_t)h->lev[l].n, st);
+        ad.emplace_back(alpha[l], (size_t)h->lev[l].n, st);
+    }
+    // device-side per-launch stats: [slot][level]
+    const int nslots = schedule == MSK_SCHED_LITERAL ? L + 1 : 1;
+    int *d_it = dalloc<int>((size_t)(nslots * L), st);
+    int *d_stat = dalloc<int>((size_t)(nslots * L), st);
+    double *d_rr = dalloc<double>((size_t)(2 * nslots * L), st);
+    MSK_CUDA(cudaMemsetAsync(d_it, 0, sizeof(int) * nslots * L, st));
+    MSK_CUDA(cudaMemsetAsync(d_stat, 0, sizeof(int) * nslots * L, st));
+    MSK_CUDA(cudaMemsetAsync(d_rr, 0, sizeof(double) * 2 * nslots * L, st));
+    unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
+    MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
+
+    int launches = 0;
+    Timer ttot(st);
+    std::vector<Timer *> cg_t, ga_t;
+    std::vector<int> cg_t_level;  // level index, or -1 for a multi-level launch
+    auto time_cg = [&](int lvl) {
+        cg_t.push_back(new Timer(st));
+        cg_t_level.push_back(lvl);
+        cg_t.back()->start();
+    };
+    auto time_ga = [&]() {
+        ga_t.push_back(new Timer(st));
+        ga_t.back()->start();
+    };
+    // B products for target level k from coefficient vectors coef[0..k-1]
+    auto b_products = [&](int k, double *const *coef_spatial, double *out_spatial) {
+        GatherArgs ga{};
+        ga.d = h->d;
+        ga.k = h->k;
+        ga.nt = h->lev[k].n;
+        for (int a = 0; a < h->d; ++a) ga.tx[a] = h->lev[k].xs + (size_t)a * h->lev[k].n;
+        ga.nlev = k;
+        for (int l = 0; l < k; ++l) ga.lev[l] = h->view(l, coef_spatial[l]);
+        ga.base = fd[k].ptr;
+        ga.base_perm = h->lev[k].perm;
+        ga.sign = -1.0;
+        ga.out = out_spatial;
+        ga.out_perm = nullptr;
+        ga.hits = d_hits;
+        time_ga();
+        gather(ga, st, &launches);
+        ga_t.back()->stop();
+    };
+
+    ttot.start();
+    std::vector<double *> alpha_sp(L), t_sp(L);
+    for (int l = 0; l < L; ++l) {
+        alpha_sp[l] = h->lev[l].alpha;
+        t_sp[l] = h->ws_t(l);
+    }
+    if (schedule == MSK_SCHED_PRUNED) {
+        // Algorithm 2 with every inner solve done once, when its input is final:
+        // beta^(l) = f^(l) - sum_{k<l} B_lk t^(k); t^(l) = A_l^{-1} beta^(l);
+        // alpha^(l) = t^(l) (the final block CG of a converged block is the
+        // same solve); the finest level is solved at tol.
+        for (int l = 0; l < L; ++l) {
+            const double tl = l + 1 < L ? inner_tol : tol;
+            CGLevelArgs a;
+            if (l == 0) {
+                a = cg_args(h, l, tl, max_iter, nullptr, fd[0].ptr, alpha_sp[l], ad[l].ptr,
+                            d_it + l, d_rr + 2 * l, d_stat + l);
+            } else {
+                b_products(l, alpha_sp.data(), h->ws_beta(l));
+                a = cg_args(h, l, tl, max_iter, h->ws_beta(l), nullptr, alpha_sp[l], ad[l].ptr,
+                            d_it + l, d_rr + 2 * l, d_stat + l);
+            }
+            time_cg(l);
+            cg_batched(&a, 1, st, &launches);
+            cg_t.back()->stop();
+        }
+    } else {
+        // Literal Algorithm 2: beta_0 = f; L sweeps of
+        //   t^(l) = A_l^{-1} beta^(l) (l < L, inner tol, one batched launch),
+        //   beta^(k) = f^(k) - sum_{l<k} B_kl t^(l)  (k >= 2)
+        // then the block-diagonal CG (Algorithm 1) on all levels at tol.
+        for (int l = 0; l < L; ++l) permute_gather(h->lev[l].n, fd[l].ptr, h->lev[l].perm, h->ws_beta(l), st, &launches);
+        for (int sweep = 0; sweep < L; ++sweep) {
+            if (L > 1) {
+                std::vector<CGLevelArgs> a;
+                for (int l = 0; l + 1 < L; ++l)
+                    a.push_back(cg_args(h, l, inner_tol, max_iter, h->ws_beta(l), nullptr, t_sp[l], nullptr,
+                                        d_it + sweep * L + l, d_rr + 2 * (sweep * L + l), d_stat + sweep * L + l));
+                time_cg(-1);
+                cg_batched(a.data(), (int)a.size(), st, &launches);
+                cg_t.back()->stop();
+                for (int k = 1; k < L; ++k) b_products(k, t_sp.data(), h->ws_beta(k));
+            }
+        }
+        std::vector<CGLevelArgs> a;
+        for (int l = 0; l < L; ++l)
+            a.push_back(cg_args(h, l, tol, max_iter, h->ws_beta(l), nullptr, alpha_sp[l], ad[l].ptr,
+                                d_it + L * L + l, d_rr + 2 * (L * L + l), d_stat + L * L + l));
+        time_cg(-1);
+        cg_batched(a.data(), L, st, &launches);
+        cg_t.back()->stop();
+    }
+    ttot.stop();
+    for (int l = 0; l < L; ++l) ad[l].flush();
+    std::vector<int> it((size_t)(nslots * L)), stat((size_t)(nslots * L));
+    std::vector<double> rr((size_t)(2 * nslots * L));
+    unsigned long long hits = 0;
+    MSK_CUDA(cudaMemcpyAsync(it.data(), d_it, sizeof(int) * it.size(), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(stat.data(), d_stat, sizeof(int) * stat.size(), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * rr.size(), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(&hits, d_hits, sizeof hits, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(d_it, st); dfree(d_stat, st); dfree(d_rr, st); dfree(d_hits, st);
+
+    msk_solve_info loc;
+    memset(&loc, 0, sizeof loc);
+    loc.L = L;
+    loc.jacobi_sweeps = schedule == MSK_SCHED_LITERAL ? L : 0;
+    const int fin = schedule == MSK_SCHED_LITERAL ? L : 0;  // slot of the final solves
+    std::string noconv;
+    for (int s = 0; s < nslots; ++s)
+        for (int l = 0; l < L; ++l) {
+            int idx = s * L + l;
+            bool used = schedule == MSK_SCHED_PRUNED || s == fin || l + 1 < L;
+            if (!used) continue;
+            if (stat[idx] && noconv.empty()) {
+                char buf[160];
+                snprintf(buf, sizeof buf, "level %d: rel. residual %.3e after %d iterations", l,
+                         rr[2 * idx + 1] > 0 ? sqrt(rr[2 * idx] / rr[2 * idx + 1]) : 0.0, it[idx]);
+                noconv = buf;
+            }
+            loc.nnz_cg += (double)it[idx] * (double)h->lev[l].nnz;
+            loc.bytes_cg += cg_bytes(h->lev[l], it[idx]);
+            if (s == fin) {
+                loc.cg_iters[l] = it[idx];
+                loc.rel_res[l] = rr[2 * idx + 1] > 0 ? sqrt(rr[2 * idx] / rr[2 * idx + 1]) : 0.0;
+                loc.bytes_cg_level[l] += cg_bytes(h->lev[l], it[idx]);
+            } else {
+                loc.inner_iters[l] += it[idx];
+            }
+        }
+    loc.nnz_gather = (double)hits;
+    for (size_t i = 0; i < cg_t.size(); ++i) {
+        double t = cg_t[i]->ms();
+        loc.t_cg_ms += t;
+        if (cg_t_level[i] >= 0) loc.t_cg_level_ms[cg_t_level[i]] += t;
+        delete cg_t[i];
+    }
+    for (auto *t : ga_t) {
+        loc.t_gather_ms += t->ms();
+        delete t;
+    }
+    loc.t_total_ms = ttot.ms();
+    loc.launches = launches;
+    if (info) *info = loc;
+    if (!noconv.empty()) throw Error(MSK_ERR_NOCONV, noconv);
+    h->solved = true;
+    API_END
+}
+
+// ================================================================ evaluate
+extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x, double *s,
+                                      msk_eval_info *info) {
+    API_BEGIN
+    require(h != nullptr, "msk_evaluate: NULL hierarchy");
+    require(m >= 0, "msk_evaluate: m < 0");
+    require(m == 0 || (x && s), "msk_evaluate: NULL argument");
+    require(m < (1ll << 31) - 1, "msk_evaluate: m too large for one call");
+    if (!h->solved) throw Error(MSK_ERR_STATE, "msk_evaluate: call msk_solve first");
+    if (info) memset(info, 0, sizeof *info);
+    if (m == 0) return MSK_OK;
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const int d = h->d, L = h->L;
+    int launches = 0;
+    Timer ttot(st), tsort(st), teval(st);
+    ttot.start();
+    DevBuf xd(x, (size_t)(m * d), st);
+    DevOut sd(s, (size_t)m, st);
+    // spatially sort the evaluation points on the finest level's grid (order
+    // only affects locality: each output is independent of it)
+    const LevelData &F = h->lev[L - 1];
+    Grid g = F.g;
+    double *xs = dalloc<double>((size_t)(m * d), st);
+    int32_t *perm = dalloc<int32_t>((size_t)m, st);
+    int32_t *cs = dalloc<int32_t>((size_t)(g.ncells + 1), st);
+    CellListOut co{};
+    co.perm = perm;
+    for (int a = 0; a < d; ++a) co.xs[a] = xs + (size_t)a * m;
+    co.cell_start = cs;
+    tsort.start();
+    build_cell_list(d, m, xd.ptr, g, false, co, st, &launches);
+    tsort.stop();
+    unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
+    MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
+    GatherArgs ga{};
+    ga.d = d;
+    ga.k = h->k;
+    ga.nt = m;
+    for (int a = 0; a < d; ++a) ga.tx[a] = xs + (size_t)a * m;
+    ga.nlev = L;
+    for (int l = 0; l < L; ++l) ga.lev[l] = h->view(l, h->lev[l].alpha);
+    ga.base = nullptr;
+    ga.sign = 1.0;
+    ga.out = sd.ptr;
+    ga.out_perm = perm;
+    ga.hits = d_hits;
+    teval.start();
+    gather(ga, st, &launches);
+    teval.stop();
+    sd.flush();
+    ttot.stop();
+    unsigned long long hits = 0;
+    MSK_CUDA(cudaMemcpyAsync(&hits, d_hits, sizeof hits, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(xs, st); dfree(perm, st); dfree(cs, st); dfree(d_hits, st);
+    if (info) {
+        info->nnz = (double)hits;
+        info->t_sort_ms = tsort.ms();
+        info->t_eval_ms = teval.ms();
+        info->t_total_ms = ttot.ms();
+        info->launches = launches;
+    }
+    API_END
+}
+
+extern "C" msk_status msk_evaluate(msk_hierarchy *h, int64_t m, const double *x, double *s) {
+    return msk_evaluate_ex(h, m, x, s, nullptr);
+}
+
+// ===================================================== row-level entry points
+extern "C" msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_level,
+                                       int64_t *row_ptr, int32_t *col, double *val) {
+    API_BEGIN
+    require(h && row_ptr, "msk_export_block: NULL argument");
+    require(row_level >= 0 && row_level < h->L && col_level >= 0 && col_level <= row_level,
+            "msk_export_block: need 0 <= col_level <= row_level < L");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const LevelData &R = h->lev[row_level], &C = h->lev[col_level];
+    const int64_t nr = R.n;
+    int32_t *cnt = nullptr;
+    int64_t *rp = nullptr;
+    int32_t *cl = nullptr;
+    double *vl = nullptr;
+    bool own = true;
+    int64_t nnz = 0;
+    if (row_level == col_level && h->assembled) {
+        rp = R.row_ptr; cl = R.col; vl = R.val; nnz = R.nnz;
+        own = false;
+    } else {
+        LevelView rv = h->view(row_level), cv = h->view(col_level);
+        cnt = dalloc<int32_t>((size_t)nr, st);
+        count_pattern(h->d, rv, cv, row_level == col_level, cnt, nullptr, st, nullptr);
+        rp = dalloc<int64_t>((size_t)(nr + 1), st);
+        exclusive_scan_i64(cnt, nr, rp, st, nullptr);
+        MSK_CUDA(cudaMemcpyAsync(&nnz, rp + nr, sizeof nnz, cudaMemcpyDeviceToHost, st));
+        MSK_CUDA(cudaStreamSynchronize(st));
+        cl = dalloc<int32_t>((size_t)nnz, st);
+        vl = dalloc<double>((size_t)nnz, st);
+        fill_pattern(h->d, h->k, rv, cv, rp, cl, vl, st, nullptr);
+    }
+    std::vector<int64_t> hrp((size_t)(nr + 1));
+    std::vector<int32_t> hcl((size_t)nnz), rperm((size_t)nr), cperm((size_t)C.n);
+    std::vector<double> hvl((size_t)nnz);
+    MSK_CUDA(cudaMemcpyAsync(hrp.data(), rp, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost, st));
+    if (nnz) {
+        MSK_CUDA(cudaMemcpyAsync(hcl.data(), cl, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
+        MSK_CUDA(cudaMemcpyAsync(hvl.data(), vl, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st));
+    }
+    MSK_CUDA(cudaMemcpyAsync(rperm.data(), R.perm, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(cperm.data(), C.perm, sizeof(int32_t) * C.n, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    if (own) { dfree(cnt, st); dfree(rp, st); dfree(cl, st); dfree(vl, st); }
+    // host re-indexing of the exported copy into caller order (diagnostic only)
+    std::vector<int64_t> inv((size_t)nr);
+    for (int64_t i = 0; i < nr; ++i) inv[rperm[i]] = i;
+    int64_t pos = 0;
+    std::vector<std::pair<int32_t, double>> tmp;
+    for (int64_t j = 0; j < nr; ++j) {
+        row_ptr[j] = pos;
+        int64_t i = inv[j];
+        tmp.clear();
+        for (int64_t p = hrp[i]; p < hrp[i + 1]; ++p) tmp.emplace_back(cperm[hcl[p]], hvl[p]);
+        std::sort(tmp.begin(), tmp.end());
+        for (auto &e : tmp) {
+            if (col) col[pos] = e.first;
+            if (val) val[pos] = e.second;
+            ++pos;
+        }
+    }
+    row_ptr[nr] = pos;
+    API_END
+}
+
+extern "C" msk_status msk_export_cells(msk_hierarchy *h, int level, int32_t *perm, int32_t *cell_start,
+                                       int64_t *cell_key, double *lo, double *cell, int64_t *dims) {
+    API_BEGIN
+    require(h != nullptr && level >= 0 && level < h->L, "msk_export_cells: bad argument");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const LevelData &D = h->lev[level];
+    std::vector<int32_t> cs((size_t)(D.g.ncells + 1));
+    MSK_CUDA(cudaMemcpyAsync(cs.data(), D.cell_start, sizeof(int32_t) * cs.size(), cudaMemcpyDeviceToHost, st));
+    if (perm) MSK_CUDA(cudaMemcpyAsync(perm, D.perm, sizeof(int32_t) * D.n, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    if (cell_start) memcpy(cell_start, cs.data(), sizeof(int32_t) * cs.size());
+    if (cell_key)
+        for (int64_t c = 0; c < D.g.ncells; ++c)
+            for (int32_t i = cs[c]; i < cs[c + 1]; ++i) cell_key[i] = c;
+    for (int a = 0; a < h->d; ++a) {
+        if (lo) lo[a] = D.g.lo[a];
+        if (dims) dims[a] = D.g.dim[a];
+    }
+    if (cell) *cell = 1.0 / D.g.inv_cell;
+    API_END
+}
+
+extern "C" msk_status msk_apply_block(msk_hierarchy *h, int row_level, int col_level, const double *v,
+                                      double *y, double *t_ms) {
+    API_BEGIN
+    require(h && v && y, "msk_apply_block: NULL argument");
+    require(row_level >= 0 && row_level < h->L && col_level >= 0 && col_level <= row_level,
+            "msk_apply_block: need 0 <= col_level <= row_level < L");
+    if (row_level == col_level && !h->assembled) throw Error(MSK_ERR_STATE, "msk_apply_block: assemble first");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const LevelData &R = h->lev[row_level], &C = h->lev[col_level];
+    DevBuf vd(v, (size_t)C.n, st);
+    DevOut yd(y, (size_t)R.n, st);
+    double *vs = dalloc<double>((size_t)C.n, st);
+    permute_gather(C.n, vd.ptr, C.perm, vs, st, nullptr);
+    Timer tm(st);
+    if (row_level == col_level) {
+        double *ys = dalloc<double>((size_t)R.n, st);
+        tm.start();
+        spmv_csr(R.n, R.row_ptr, R.col, R.val, vs, ys, st, nullptr);
+        tm.stop();
+        permute_scatter(R.n, ys, R.perm, yd.ptr, st, nullptr);
+        dfree(ys, st);
+    } else {
+        GatherArgs ga{};
+        ga.d = h->d;
+        ga.k = h->k;
+        ga.nt = R.n;
+        for (int a = 0; a < h->d; ++a) ga.tx[a] = R.xs + (size_t)a * R.n;
+        ga.nlev = 1;
+        ga.lev[0] = h->view(col_level, vs);
+        ga.sign = 1.0;
+        ga.out = yd.ptr;
+        ga.out_perm = R.perm;
+        tm.start();
+        gather(ga, st, nullptr);
+        tm.stop();
+    }
+    yd.flush();
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(vs, st);
+    if (t_ms) *t_ms = tm.ms();
+    API_END
+}
+
+extern "C" msk_status msk_cg_level(msk_hierarchy *h, int level, const double *b, double *x, double tol,
+                                   int32_t max_iter, int32_t *iters, double *rel_res, double *t_ms) {
+    API_BEGIN
+    require(h && b && x, "msk_cg_level: NULL argument");
+    require(level >= 0 && level < h->L, "msk_cg_level: bad level");
+    require(tol > 0.0 && tol < 1.0 && max_iter >= 1, "msk_cg_level: bad tol / max_iter");
+    if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_cg_level: assemble first");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    h->ensure_ws();
+    const LevelData &D = h->lev[level];
+    DevBuf bd(b, (size_t)D.n, st);
+    DevOut xd(x, (size_t)D.n, st);
+    double *xs = dalloc<double>((size_t)D.n, st);
+    int *d_it = dalloc<int>(2, st);
+    double *d_rr = dalloc<double>(2, st);
+    CGLevelArgs a = cg_args(h, level, tol, max_iter, nullptr, bd.ptr, xs, xd.ptr, d_it, d_rr, d_it + 1);
+    Timer tm(st);
+    tm.start();
+    cg_batched(&a, 1, st, nullptr);
+    tm.stop();
+    xd.flush();
+    int hit[2];
+    double hrr[2];
+    MSK_CUDA(cudaMemcpyAsync(hit, d_it, sizeof hit, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(hrr, d_rr, sizeof hrr, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(xs, st); dfree(d_it, st); dfree(d_rr, st);
+    if (iters) *iters = hit[0];
+    if (rel_res) *rel_res = hrr[1] > 0 ? sqrt(hrr[0] / hrr[1]) : 0.0;
+    if (t_ms) *t_ms = tm.ms();
+    if (hit[1]) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "level %d: rel. residual %.3e after %d iterations", level,
+                 hrr[1] > 0 ? sqrt(hrr[0] / hrr[1]) : 0.0, hit[0]);
+        throw Error(MSK_ERR_NOCONV, buf);
+    }
+    API_END
+}
+
+extern "C" const char *msk_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char *msk_version(void) { return "libmsk 0.1 (sm_100a, FP64)"; }

@@ -1,0 +1,125 @@
+// common.cuh -- shared device helpers of libmsk (sm_100a, FP64).
+//
+// Nothing here is shared with oracle/ (which is independent test code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace msk {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+
+#define MSK_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::msk::Error(e_ == cudaErrorMemoryAllocation ? 2 : 3,                   \
+                               std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+#define MSK_CHECK_LAUNCH() MSK_CUDA(cudaGetLastError())
+
+constexpr int kMaxLevels = 16;
+
+// ---------------------------------------------------------------- geometry
+// Uniform grid of one level: cell side c >= delta (1 + 2^-20), row-major
+// x-major keys key = (ix * ny + iy) * nz + iz (nz = 1 in 2-D).  A pair with
+// r < delta lies in cells whose indices differ by at most 1 per axis
+// (DESIGN.md "Cell list").
+struct Grid {
+    double lo[3];
+    double inv_cell;
+    int64_t dim[3];  // nx, ny, nz (nz = 1 for d = 2)
+    int64_t ncells;
+};
+
+// One level as seen by the device kernels (points in spatial order, SoA).
+struct LevelView {
+    int64_t n;
+    const double *x[3];         // SoA coordinates, spatial order
+    const int32_t *cell_start;  // ncells + 1
+    Grid g;
+    double delta2;              // delta * delta, computed once on the host (reading C-4)
+    double inv_delta;           // 1 / delta
+    double scale;               // delta^-d
+    const double *coef;         // coefficient vector (spatial order) for gathers
+};
+
+// squared distance, left to right, round-to-nearest, no FMA (reading C-4)
+template <int D>
+__device__ __forceinline__ double dist2_nofma(const double *a, const double *b) {
+    double t = __dsub_rn(a[0], b[0]);
+    double s = __dmul_rn(t, t);
+    t = __dsub_rn(a[1], b[1]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+    if (D == 3) {
+        t = __dsub_rn(a[2], b[2]);
+        s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    return s;
+}
+
+// Wendland phi_{d,k}(r) for d in {2,3}: l = floor(d/2) + k + 1 = k + 2
+// (reading C-3; P:1275 for k = 1).  Valid for 0 <= r < 1.
+template <int K>
+__device__ __forceinline__ double wendland(double r) {
+    double s = fmax(1.0 - r, 0.0);  // r*inv_delta may round to 1 + ulp at the boundary
+    double s2 = s * s;
+    if (K == 0) return s2;
+    if (K == 1) return (s2 * s2) * fma(4.0, r, 1.0);
+    // K == 2
+    double s6 = s2 * s2 * s2;
+    return s6 * fma(fma(35.0, r, 18.0), r, 3.0) * (1.0 / 3.0);
+}
+
+// cell coordinate of x along axis a, not clamped
+__device__ __forceinline__ int64_t cell_coord(const Grid &g, int a, double x) {
+    return (int64_t)floor(__dmul_rn(__dsub_rn(x, g.lo[a]), g.inv_cell));
+}
+
+// --------------------------------------------------------- reductions
+// Deterministic block sum: fixed xor-shuffle tree per warp, warp partials
+// summed in warp order by warp 0.  Result valid in all threads.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *smem /* >= NT/32 + 1 */) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) smem[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double t = lane < NT / 32 ? smem[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) smem[NT / 32] = t;
+    }
+    __syncthreads();
+    return smem[NT / 32];
+}
+
+template <int NT>
+__device__ __forceinline__ long long block_sum_ll(long long v, long long *smem) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) smem[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        long long t = lane < NT / 32 ? smem[lane] : 0;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) smem[NT / 32] = t;
+    }
+    __syncthreads();
+    return smem[NT / 32];
+}
+
+inline unsigned ceil_div_u(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace msk
