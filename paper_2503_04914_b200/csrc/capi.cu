@@ -45,6 +45,7 @@ struct LevelData {
     int32_t *col = nullptr;
     double *val = nullptr;
     double *alpha = nullptr;       // coefficients of the last solve, spatial order
+    double4 *rec = nullptr;        // packed (coords, coefficient) records for gathers
 };
 
 thread_local std::string g_err;
@@ -191,7 +192,15 @@ struct msk_hierarchy {
         v.inv_delta = 1.0 / D.delta;
         v.scale = pow(D.delta, -(double)d);
         v.coef = coef;
+        v.rec = D.rec;
         return v;
+    }
+
+    // pack level l's coordinates with coefficient vector coef (spatial order)
+    void pack(int l, const double *coef, int *launches) {
+        LevelData &D = lev[l];
+        if (!D.rec) D.rec = dalloc<double4>((size_t)D.n, st());
+        pack_records(D.n, d, D.xs, coef, D.rec, st(), launches);
     }
 
     void ensure_ws() {
@@ -208,7 +217,7 @@ struct msk_hierarchy {
         for (int l = 0; l < L; ++l) {
             LevelData &D = lev[l];
             dfree(D.xs, s); dfree(D.perm, s); dfree(D.cell_start, s); dfree(D.cnt, s);
-            dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s);
+            dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s); dfree(D.rec, s);
             D = LevelData();
         }
         dfree(ws, s);
@@ -417,7 +426,8 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
     for (int l = 0; l < h->L; ++l) {
         LevelData &D = h->lev[l];
         dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st);
-        D.row_ptr = dalloc<int64_t>((size_t)(D.n + 1), st);
+        D.row_ptr = dalloc<int64_t>((size_t)(D.n + 3), st);  // + padding for 16-byte bulk copies
+        MSK_CUDA(cudaMemsetAsync(D.row_ptr + D.n + 1, 0, 2 * sizeof(int64_t), st));
         exclusive_scan_i64(D.cnt, D.n, D.row_ptr, st, &launches);
         MSK_CUDA(cudaMemcpyAsync(&nnz[l], D.row_ptr + D.n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     }
@@ -425,8 +435,10 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
     for (int l = 0; l < h->L; ++l) {
         LevelData &D = h->lev[l];
         D.nnz = nnz[l];
-        D.col = dalloc<int32_t>((size_t)D.nnz, st);
-        D.val = dalloc<double>((size_t)D.nnz, st);
+        D.col = dalloc<int32_t>((size_t)D.nnz + 4, st);  // + padding for 16-byte bulk copies
+        D.val = dalloc<double>((size_t)D.nnz + 2, st);
+        MSK_CUDA(cudaMemsetAsync(D.col + D.nnz, 0, 4 * sizeof(int32_t), st));
+        MSK_CUDA(cudaMemsetAsync(D.val + D.nnz, 0, 2 * sizeof(double), st));
         LevelView v = h->view(l);
         fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
     }
@@ -476,9 +488,10 @@ CGLevelArgs cg_args(msk_hierarchy *h, int l, double tol, int max_iter, const dou
 }
 
 double cg_bytes(const LevelData &D, int iters) {
-    // algorithmic bytes (DESIGN.md §Roofline): per iteration 12 B/nnz (val + col)
-    // + 96 B/row (row_ptr 8, gathered p 8, q 8, x/r/p/q updates 72); init 32 B/row
-    return (double)iters * (12.0 * (double)D.nnz + 96.0 * (double)D.n) + 32.0 * (double)D.n;
+    // algorithmic bytes (DESIGN.md §7): per iteration 12 B/nnz (val + col)
+    // + 88 B/row (row_ptr 8, gathered p 8, q write 8, r-phase 24, x/p-phase 40);
+    // init 32 B/row (b read; x, r, p written)
+    return (double)iters * (12.0 * (double)D.nnz + 88.0 * (double)D.n) + 32.0 * (double)D.n;
 }
 
 }  // namespace
@@ -578,6 +591,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             time_cg(l);
             cg_batched(&a, 1, st, &launches);
             cg_t.back()->stop();
+            if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);  // source records for later B products
         }
     } else {
         // Literal Algorithm 2: beta_0 = f; L sweeps of
@@ -594,6 +608,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 time_cg(-1);
                 cg_batched(a.data(), (int)a.size(), st, &launches);
                 cg_t.back()->stop();
+                for (int l = 0; l + 1 < L; ++l) h->pack(l, t_sp[l], &launches);
                 for (int k = 1; k < L; ++k) b_products(k, t_sp.data(), h->ws_beta(k));
             }
         }
@@ -704,6 +719,7 @@ extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double 
     ga.nt = m;
     for (int a = 0; a < d; ++a) ga.tx[a] = xs + (size_t)a * m;
     ga.nlev = L;
+    for (int l = 0; l < L; ++l) h->pack(l, h->lev[l].alpha, &launches);
     for (int l = 0; l < L; ++l) ga.lev[l] = h->view(l, h->lev[l].alpha);
     ga.base = nullptr;
     ga.sign = 1.0;
@@ -850,6 +866,7 @@ extern "C" msk_status msk_apply_block(msk_hierarchy *h, int row_level, int col_l
         ga.nt = R.n;
         for (int a = 0; a < h->d; ++a) ga.tx[a] = R.xs + (size_t)a * R.n;
         ga.nlev = 1;
+        h->pack(col_level, vs, nullptr);
         ga.lev[0] = h->view(col_level, vs);
         ga.sign = 1.0;
         ga.out = yd.ptr;

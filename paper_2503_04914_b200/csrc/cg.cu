@@ -10,39 +10,61 @@
 //
 //   x = 0, r = b, p = b, bb = rr = b.b
 //   while rr > tol^2 bb and it < max_iter:          (reading C-9)
-//       q = A p ; pq = p.q          -- CSR-stream SpMV fused with the dot
+//       q = A p ; pq = p.q            -- SpMV fused with the dot      [barrier]
 //       alpha = rr / pq
-//       x += alpha p ; r -= alpha q ; rr' = r.r      -- fused update + dot
-//       beta = rr' / rr ; p = r + beta p
+//       r -= alpha q ; rr' = r.r      -- fused update + dot           [barrier]
+//       beta = rr' / rr
+//       x += alpha p ; p = r + beta p -- x update deferred to here    [barrier]
 //
-// SpMV (CSR-stream): a CTA takes a tile of NT consecutive rows (spatial
-// order), streams the tile's contiguous nnz range with fully coalesced loads
-// of val/col, gathers p[col] (L2-resident thanks to the spatial sort) and
-// stages the products in shared memory; each thread then sums its row in
+// SpMV: a CTA takes a tile of NT consecutive rows (spatial order).  One
+// thread streams the tile's contiguous CSR slices (values, columns) into
+// shared memory with a bulk-async copy (TMA, cp.async.bulk, L2 evict-first
+// so the gathered vector p stays L2-resident) completing on an mbarrier; the
+// threads then only issue the irregular gathers p[col] (8 independent loads
+// in flight per thread), multiply in place, and each thread sums its row in
 // ascending column order (deterministic).
 //
-// Reductions: fixed xor-shuffle tree per warp -> fixed warp order -> one
-// partial per CTA -> after the group barrier every CTA sums the partials in
-// the same fixed order.  All CTAs of a group therefore hold bit-identical
-// scalars and take identical control flow; results do not depend on timing.
-#include <cooperative_groups.h>
+// Work unit and reductions: a level's tiles are grouped into chunks of CH
+// tiles (CH fixed by n alone); chunk c belongs to CTA c mod nb.  Each chunk
+// writes one partial per dot product (fixed xor-shuffle tree per warp ->
+// fixed warp order); after the group barrier every CTA sums all chunk
+// partials in the same fixed order.  The result therefore depends only on n,
+// not on the number of CTAs, the GPU or the other levels of the batch, and
+// all CTAs of a group take identical control flow.
 #include <cuda/atomic>
 
 #include <vector>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace msk {
 
 namespace {
-constexpr int NT = 256;     // threads per CTA == rows per tile
-constexpr int CAP = 4096;   // staged products per chunk (32 KB of shared memory)
-constexpr int U = 4;        // independent gathers in flight per thread
-constexpr int CH = 4;       // tiles per reduction chunk (the unit of work distribution)
+constexpr int NT = 256;       // threads per CTA == rows per tile
+constexpr int NW = NT / 32;   // warps per CTA
+constexpr int CAPW = 320;     // CSR entries per warp pipeline stage (values 2.5 KB + columns 1.3 KB)
+constexpr int CAPWE = CAPW - 2;  // usable entries per stage (16-byte alignment slack)
+constexpr int U = 8;          // independent gathers in flight per lane
+constexpr int MAXCH = 4;      // max tiles per chunk
+constexpr int RPCAP = MAXCH * NT + 4;  // staged row pointers per chunk
 
 struct CGBatch {
     int nlev;
     CGLevelArgs lev[kMaxLevels];
+};
+
+struct __align__(16) WarpStage {
+    double val[CAPW];         // values, overwritten in place by the products
+    int32_t col[CAPW + 8];
+};
+
+struct __align__(16) CGShared {
+    WarpStage st[NW][2];      // per-warp double-buffered CSR slices
+    int64_t rp[RPCAP];        // row pointers of the current chunk
+    double red[NT / 32 + 2];
+    uint64_t bar;             // CTA barrier for the row-pointer copy
+    uint64_t wbar[NW][2];     // per-warp, per-stage barriers
 };
 
 __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
@@ -56,7 +78,7 @@ __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
             a.fetch_add(1ull, cuda::memory_order_release);
             unsigned long long spins = 0;
             while (a.load(cuda::memory_order_acquire) < round) {
-                __nanosleep(64);
+                __nanosleep(32);
                 if (++spins > (1ull << 31)) __trap();  // never hang the device forever
             }
             __threadfence();
@@ -65,12 +87,8 @@ __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
     }
 }
 
-// Deterministic all-reduce over the chunk partials of one group.  Each chunk
-// (CH consecutive tiles) is owned by exactly one CTA, which has written its
-// partial; after the group barrier every CTA sums all partials in the same
-// fixed order.  The result depends only on n (not on the number of CTAs in
-// the group or on the GPU), so a level gives bit-identical results whether
-// it is solved alone or batched with other levels.
+// Deterministic all-reduce over the chunk partials of one group: after the
+// group barrier every CTA sums all partials in the same fixed order.
 __device__ __forceinline__ double chunk_allreduce(const double *partials, int64_t nchunks, int nb,
                                                   unsigned long long *ctr,
                                                   unsigned long long &round, double *s_red) {
@@ -80,48 +98,157 @@ __device__ __forceinline__ double chunk_allreduce(const double *partials, int64_
     return block_sum<NT>(t, s_red);
 }
 
-// q = A p on rows [r0, r0+nr); returns this thread's q (row r0+tid) or 0.
-__device__ __forceinline__ double spmv_tile(int64_t r0, int nr, const int64_t *__restrict__ row_ptr,
-                                            const int32_t *__restrict__ col,
-                                            const double *__restrict__ val, const double *p,
-                                            double *s_prod, int64_t *s_rp) {
-    const int tid = threadIdx.x;
-    for (int t = tid; t <= nr; t += NT) s_rp[t] = __ldg(&row_ptr[r0 + t]);
-    __syncthreads();
-    const int64_t k0 = s_rp[0], k1 = s_rp[nr];
-    int64_t myb = 0, mye = 0;
-    if (tid < nr) { myb = s_rp[tid]; mye = s_rp[tid + 1]; }
-    double acc = 0.0;
-    for (int64_t cb = k0; cb < k1; cb += CAP) {
-        const int64_t ce = cb + CAP < k1 ? cb + CAP : k1;
-        for (int64_t k = cb + tid; k < ce; k += NT * U) {
-            double v[U];
-            int c[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                int64_t kk = k + (int64_t)u * NT;
-                if (kk < ce) { v[u] = __ldg(&val[kk]); c[u] = __ldg(&col[kk]); }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                int64_t kk = k + (int64_t)u * NT;
-                if (kk < ce) s_prod[kk - cb] = v[u] * p[c[u]];
-            }
-        }
-        __syncthreads();
-        if (tid < nr) {
-            int64_t lo = myb > cb ? myb : cb, hi = mye < ce ? mye : ce;
-            for (int64_t k = lo; k < hi; ++k) acc += s_prod[k - cb];
-        }
-        __syncthreads();
+// Stage row pointers of rows [r0, r0 + nrows] (nrows + 1 entries) into
+// S.rp; returns the offset of row r0 inside S.rp.  Whole CTA calls.
+__device__ __forceinline__ int stage_row_ptr(CGShared &S, const int64_t *row_ptr, int64_t r0,
+                                             int nrows, uint32_t &phase, uint64_t pol) {
+    const int64_t lo = r0 & ~(int64_t)1;
+    const int64_t hi = (r0 + nrows + 2) & ~(int64_t)1;  // exclusive, even
+    if (threadIdx.x == 0) {
+        uint32_t bytes = (uint32_t)((hi - lo) * 8);
+        mbar_arrive_expect_tx(&S.bar, bytes);
+        tma_load_1d(S.rp, row_ptr + lo, bytes, &S.bar, pol);
     }
-    return acc;
+    mbar_wait(&S.bar, phase);
+    phase ^= 1u;
+    return (int)(r0 - lo);
 }
 
-__global__ void __launch_bounds__(NT, 4) k_cg(CGBatch B) {
-    __shared__ double s_prod[CAP];
-    __shared__ int64_t s_rp[NT + 1];
-    __shared__ double s_red[NT / 32 + 2];
+// Issue the bulk copies of CSR entries [kb, ke) into a warp stage (lane 0).
+__device__ __forceinline__ void issue_piece(WarpStage &stg, uint64_t *bar, const int32_t *col,
+                                            const double *val, int64_t kb, int64_t ke,
+                                            uint64_t pol) {
+    const int64_t vlo = kb & ~(int64_t)1, vhi = (ke + 1) & ~(int64_t)1;
+    const int64_t clo = kb & ~(int64_t)3, chi = (ke + 3) & ~(int64_t)3;
+    const uint32_t vb = (uint32_t)((vhi - vlo) * 8), cb = (uint32_t)((chi - clo) * 4);
+    mbar_arrive_expect_tx(bar, vb + cb);
+    tma_load_1d(stg.val, val + vlo, vb, bar, pol);
+    tma_load_1d(stg.col, col + clo, cb, bar, pol);
+}
+
+// Warp-level pipelined SpMV: q_i = (A p)_i for the warp's rows
+// [wr0, wr0 + nrows) whose row pointers sit at S.rp[ro ...].  The rows are
+// cut into subtiles of 32 (lane == row) and the subtiles' CSR slices into
+// pieces of <= CAPWE entries; piece j+1 is copied (TMA) into the other
+// stage while piece j is processed.  Lanes gather p[col] for the piece's
+// entries (strided, U loads in flight), multiply in place, then each lane
+// sums its own row in ascending column order.  Returns the lane's share
+// of p.q over its rows.  J counts the warp's pieces over the whole launch:
+// piece J uses stage J&1 and completes its barrier phase with parity
+// (J>>1)&1.
+__device__ __forceinline__ double spmv_warp(CGShared &S, int ro, int nrows, int64_t wr0,
+                                            const int32_t *col, const double *val, const double *p,
+                                            double *q, uint32_t &J, uint64_t pol) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpStage *stg = S.st[w];
+    uint64_t *bars = S.wbar[w];
+    double dot = 0.0;
+    if (nrows <= 0) return 0.0;
+    const int nsub = (nrows + 31) >> 5;
+    // piece cursor: subtile s, entries [kb, ke)
+    int s = 0;
+    int64_t sub_end = S.rp[ro + (nrows < 32 ? nrows : 32)];
+    int64_t kb = S.rp[ro];
+    int64_t ke = kb + CAPWE < sub_end ? kb + CAPWE : sub_end;
+    if (lane == 0) issue_piece(stg[J & 1], &bars[J & 1], col, val, kb, ke, pol);
+    int64_t myb = lane < nrows ? S.rp[ro + lane] : 0, mye = lane < nrows ? S.rp[ro + lane + 1] : 0;
+    double acc = 0.0;
+    for (uint32_t j = J;; ++j) {
+        // next piece
+        int s2 = s;
+        int64_t kb2 = ke, ke2 = 0, sub_end2 = sub_end;
+        if (ke == sub_end) {
+            s2 = s + 1;
+            if (s2 < nsub) {
+                int re = (s2 + 1) * 32 < nrows ? (s2 + 1) * 32 : nrows;
+                sub_end2 = S.rp[ro + re];
+            }
+        }
+        const bool has_next = s2 < nsub;
+        if (has_next) ke2 = kb2 + CAPWE < sub_end2 ? kb2 + CAPWE : sub_end2;
+        // stage (j+1)&1 held piece j-1, fully consumed (fence + syncwarp at its end)
+        if (has_next && lane == 0) issue_piece(stg[(j + 1) & 1], &bars[(j + 1) & 1], col, val, kb2, ke2, pol);
+        const int sj = (int)(j & 1u);
+        mbar_wait(&bars[sj], (j >> 1) & 1u);
+        WarpStage &cur = stg[sj];
+        const int voff = (int)(kb & 1), coff = (int)(kb & 3), m = (int)(ke - kb);
+        for (int e = lane; e < m; e += 32 * U) {
+            double pv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                int ee = e + u * 32;
+                pv[u] = ee < m ? p[cur.col[coff + ee]] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                int ee = e + u * 32;
+                if (ee < m) cur.val[voff + ee] *= pv[u];
+            }
+        }
+        __syncwarp();
+        {
+            int64_t lo = myb > kb ? myb : kb, hi = mye < ke ? mye : ke;
+            for (int64_t k = lo; k < hi; ++k) acc += cur.val[voff + (int)(k - kb)];
+        }
+        if (ke == sub_end) {  // subtile s complete
+            const int lr = s * 32 + lane;
+            if (lr < nrows) {
+                const int64_t i = wr0 + lr;
+                q[i] = acc;
+                dot += p[i] * acc;
+            }
+            acc = 0.0;
+            if (has_next) {
+                const int lr2 = s2 * 32 + lane;
+                myb = lr2 < nrows ? S.rp[ro + lr2] : 0;
+                mye = lr2 < nrows ? S.rp[ro + lr2 + 1] : 0;
+            }
+        }
+        fence_proxy_async_smem();  // generic writes to this stage before its next TMA refill
+        __syncwarp();
+        if (!has_next) {
+            J = j + 1;
+            break;
+        }
+        s = s2;
+        kb = kb2;
+        ke = ke2;
+        sub_end = sub_end2;
+    }
+    return dot;
+}
+
+__device__ __forceinline__ void init_barriers(CGShared &S) {
+    if ((threadIdx.x & 31) == 0) {
+        const int w = threadIdx.x >> 5;
+        mbar_init(&S.wbar[w][0], 1);
+        mbar_init(&S.wbar[w][1], 1);
+        if (w == 0) mbar_init(&S.bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+// q = A p over one chunk of rows [cr0, cr0 + crows): row pointers staged by
+// the CTA, then each warp runs its pipelined SpMV over its contiguous rows.
+// Returns the thread's share of p.q.
+__device__ __forceinline__ double spmv_chunk(CGShared &S, const int64_t *row_ptr, const int32_t *col,
+                                             const double *val, const double *p, double *q,
+                                             int64_t cr0, int crows, int CH, uint32_t &phase,
+                                             uint32_t &J, uint64_t pol) {
+    const int ro = stage_row_ptr(S, row_ptr, cr0, crows, phase, pol);
+    const int w = threadIdx.x >> 5;
+    const int per = 32 * CH;
+    const int w0 = w * per;
+    const int wn = crows - w0 < per ? crows - w0 : per;
+    double dot = spmv_warp(S, ro + w0, wn, cr0 + w0, col, val, p, q, J, pol);
+    __syncthreads();  // S.rp is reused by the next chunk's copy
+    return dot;
+}
+
+__global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CGShared &S = *reinterpret_cast<CGShared *>(smem_raw);
 
     int g = 0;
     while (g + 1 < B.nlev && (int)blockIdx.x >= B.lev[g + 1].block_begin) ++g;
@@ -129,35 +256,33 @@ __global__ void __launch_bounds__(NT, 4) k_cg(CGBatch B) {
     const int nb = L.nblocks, me = (int)blockIdx.x - L.block_begin;
     const int tid = threadIdx.x;
     const int64_t n = L.n;
+    const int CH = L.chunk_tiles;
     const int64_t ntiles = (n + NT - 1) / NT;
     const int64_t nchunks = (ntiles + CH - 1) / CH;
-    double *__restrict__ x = L.x;
-    double *__restrict__ r = L.r;
-    double *p = L.p;  // written by other CTAs between barriers: plain (coherent) loads
-    double *__restrict__ q = L.q;
     double *part = L.partials;  // 3 * nchunks
     unsigned long long round = 0;
-    // chunk c = tiles [c*CH, min((c+1)*CH, ntiles)), owned by CTA c mod nb
-#define MSK_FOR_CHUNK_TILES(c, t) \
-    for (int64_t t = (c) * CH, t##_e = ((c) + 1) * CH < ntiles ? ((c) + 1) * CH : ntiles; t < t##_e; ++t)
+    uint32_t phase = 0;
+    uint32_t J = 0;  // pieces consumed by this warp
+    init_barriers(S);
+    const uint64_t pol = policy_evict_first();
 
     // ---- init: x = 0, r = p = b, bb = b.b
     for (int64_t c = me; c < nchunks; c += nb) {
         double acc = 0.0;
-        MSK_FOR_CHUNK_TILES(c, t) {
-            int64_t i = t * NT + tid;
+        for (int t = 0; t < CH; ++t) {
+            int64_t i = (c * CH + t) * NT + tid;
             if (i < n) {
                 double bi = L.b_src ? __ldg(&L.b_src[__ldg(&L.b_perm[i])]) : __ldg(&L.b[i]);
-                x[i] = 0.0;
-                r[i] = bi;
-                p[i] = bi;
+                L.x[i] = 0.0;
+                L.r[i] = bi;
+                L.p[i] = bi;
                 acc += bi * bi;
             }
         }
-        double s = block_sum<NT>(acc, s_red);
+        double s = block_sum<NT>(acc, S.red);
         if (tid == 0) part[c] = s;
     }
-    const double bb = chunk_allreduce(part, nchunks, nb, L.barrier, round, s_red);
+    const double bb = chunk_allreduce(part, nchunks, nb, L.barrier, round, S.red);
     double rr = bb;
     int it = 0, status = 0;
     if (bb > 0.0) {
@@ -166,46 +291,72 @@ __global__ void __launch_bounds__(NT, 4) k_cg(CGBatch B) {
             if (rr <= stop) break;
             if (it >= L.max_iter) { status = 1; break; }
             // ---- q = A p, pq = p.q
-            for (int64_t c = me; c < nchunks; c += nb) {
-                double acc = 0.0;
-                MSK_FOR_CHUNK_TILES(c, t) {
-                    int64_t r0 = t * NT;
-                    int nr = (int)(n - r0 < NT ? n - r0 : NT);
-                    double qi = spmv_tile(r0, nr, L.row_ptr, L.col, L.val, p, s_prod, s_rp);
-                    if (tid < nr) {
-                        q[r0 + tid] = qi;
-                        acc += p[r0 + tid] * qi;
-                    }
+            {
+                const double *p = L.p;  // written by other CTAs in earlier phases: coherent loads
+                for (int64_t c = me; c < nchunks; c += nb) {
+                    const int64_t cr0 = c * CH * NT;
+                    const int crows = (int)(n - cr0 < (int64_t)CH * NT ? n - cr0 : (int64_t)CH * NT);
+                    double acc = spmv_chunk(S, L.row_ptr, L.col, L.val, p, L.q, cr0, crows, CH, phase,
+                                            J, pol);
+                    double s = block_sum<NT>(acc, S.red);
+                    if (tid == 0) part[nchunks + c] = s;
                 }
-                double s = block_sum<NT>(acc, s_red);
-                if (tid == 0) part[nchunks + c] = s;
             }
-            const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, s_red);
+            const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, S.red);
             const double alpha = rr / pq;
-            // ---- x += alpha p, r -= alpha q, rr' = r.r
-            for (int64_t c = me; c < nchunks; c += nb) {
-                double acc = 0.0;
-                MSK_FOR_CHUNK_TILES(c, t) {
-                    int64_t i = t * NT + tid;
-                    if (i < n) {
-                        double pi = p[i];
-                        x[i] += alpha * pi;
-                        double ri = r[i] - alpha * q[i];
-                        r[i] = ri;
-                        acc += ri * ri;
+            // ---- r -= alpha q, rr' = r.r
+            {
+                double *__restrict__ r = L.r;
+                const double *__restrict__ q = L.q;
+                for (int64_t c = me; c < nchunks; c += nb) {
+                    double rv[MAXCH], qv[MAXCH];
+#pragma unroll
+                    for (int t = 0; t < MAXCH; ++t) {
+                        int64_t i = (c * CH + t) * NT + tid;
+                        bool ok = t < CH && i < n;
+                        rv[t] = ok ? r[i] : 0.0;
+                        qv[t] = ok ? q[i] : 0.0;
                     }
+                    double acc = 0.0;
+#pragma unroll
+                    for (int t = 0; t < MAXCH; ++t) {
+                        int64_t i = (c * CH + t) * NT + tid;
+                        if (t < CH && i < n) {
+                            double ri = rv[t] - alpha * qv[t];
+                            r[i] = ri;
+                            acc += ri * ri;
+                        }
+                    }
+                    double s = block_sum<NT>(acc, S.red);
+                    if (tid == 0) part[2 * nchunks + c] = s;
                 }
-                double s = block_sum<NT>(acc, s_red);
-                if (tid == 0) part[2 * nchunks + c] = s;
             }
-            const double rrn = chunk_allreduce(part + 2 * nchunks, nchunks, nb, L.barrier, round, s_red);
+            const double rrn = chunk_allreduce(part + 2 * nchunks, nchunks, nb, L.barrier, round, S.red);
             const double beta = rrn / rr;
             rr = rrn;
-            // ---- p = r + beta p
-            for (int64_t c = me; c < nchunks; c += nb) {
-                MSK_FOR_CHUNK_TILES(c, t) {
-                    int64_t i = t * NT + tid;
-                    if (i < n) p[i] = r[i] + beta * p[i];
+            // ---- x += alpha p, p = r + beta p
+            {
+                double *__restrict__ x = L.x;
+                double *__restrict__ p = L.p;
+                const double *__restrict__ r = L.r;
+                for (int64_t c = me; c < nchunks; c += nb) {
+                    double xv[MAXCH], pv[MAXCH], rv[MAXCH];
+#pragma unroll
+                    for (int t = 0; t < MAXCH; ++t) {
+                        int64_t i = (c * CH + t) * NT + tid;
+                        bool ok = t < CH && i < n;
+                        xv[t] = ok ? x[i] : 0.0;
+                        pv[t] = ok ? p[i] : 0.0;
+                        rv[t] = ok ? r[i] : 0.0;
+                    }
+#pragma unroll
+                    for (int t = 0; t < MAXCH; ++t) {
+                        int64_t i = (c * CH + t) * NT + tid;
+                        if (t < CH && i < n) {
+                            x[i] = xv[t] + alpha * pv[t];
+                            p[i] = rv[t] + beta * pv[t];
+                        }
+                    }
                 }
             }
             group_barrier(L.barrier, nb, round);
@@ -213,14 +364,12 @@ __global__ void __launch_bounds__(NT, 4) k_cg(CGBatch B) {
         }
     }
     if (L.x_out) {
-        for (int64_t c = me; c < nchunks; c += nb) {
-            MSK_FOR_CHUNK_TILES(c, t) {
-                int64_t i = t * NT + tid;
-                if (i < n) L.x_out[__ldg(&L.x_perm[i])] = x[i];
+        for (int64_t c = me; c < nchunks; c += nb)
+            for (int t = 0; t < CH; ++t) {
+                int64_t i = (c * CH + t) * NT + tid;
+                if (i < n) L.x_out[__ldg(&L.x_perm[i])] = L.x[i];
             }
-        }
     }
-#undef MSK_FOR_CHUNK_TILES
     if (me == 0 && tid == 0) {
         *L.out_iters = it;
         L.out_rr[0] = rr;
@@ -229,30 +378,50 @@ __global__ void __launch_bounds__(NT, 4) k_cg(CGBatch B) {
     }
 }
 
+// standalone y = A v (msk_apply_block): one CTA per tile
 __global__ void __launch_bounds__(NT) k_spmv(int64_t n, const int64_t *__restrict__ row_ptr,
                                              const int32_t *__restrict__ col,
                                              const double *__restrict__ val,
                                              const double *__restrict__ v, double *__restrict__ y) {
-    __shared__ double s_prod[CAP];
-    __shared__ int64_t s_rp[NT + 1];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CGShared &S = *reinterpret_cast<CGShared *>(smem_raw);
+    uint32_t phase = 0;
+    uint32_t J = 0;  // pieces consumed by this warp
+    init_barriers(S);
+    const uint64_t pol = policy_evict_first();
     int64_t r0 = (int64_t)blockIdx.x * NT;
     int nr = (int)(n - r0 < NT ? n - r0 : NT);
-    double qi = spmv_tile(r0, nr, row_ptr, col, val, v, s_prod, s_rp);
-    if ((int)threadIdx.x < nr) y[r0 + threadIdx.x] = qi;
+    spmv_chunk(S, row_ptr, col, val, v, y, r0, nr, 1, phase, J, pol);
 }
 
 int g_max_resident = 0;
+
+void set_smem_attrs() {
+    static bool done = false;
+    if (done) return;
+    MSK_CUDA(cudaFuncSetAttribute(k_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
+    MSK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
+    done = true;
+}
 }  // namespace
 
 int cg_max_resident_blocks() {
     if (g_max_resident == 0) {
+        set_smem_attrs();
         int dev = 0, sms = 0, per = 0;
         MSK_CUDA(cudaGetDevice(&dev));
         MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg, NT, 0));
+        MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg, NT, sizeof(CGShared)));
         g_max_resident = sms * (per > 0 ? per : 1);
     }
     return g_max_resident;
+}
+
+// tiles per chunk: a function of n only (keeps results launch-independent);
+// large levels use larger chunks to bound the partial-sum traffic
+int cg_chunk_tiles(int64_t n) {
+    int64_t tiles = (n + NT - 1) / NT;
+    return tiles >= 16384 ? 4 : 1;
 }
 
 // levels[i].nblocks == 0 => the launcher assigns CTAs proportionally to work.
@@ -266,15 +435,19 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     for (int l = 0; l < nlev; ++l) {
         work[l] = (double)levels[l].nnz + 12.0 * (double)levels[l].n;  // ~bytes/8 per iteration
         wsum += work[l];
+        for (const void *ptr : {(const void *)levels[l].row_ptr, (const void *)levels[l].col,
+                                (const void *)levels[l].val})
+            if (((uintptr_t)ptr & 15u) != 0) throw Error(3, "cg_batched: CSR arrays must be 16-byte aligned");
     }
     // CTA allocation: proportional to work, at least one, at most one per chunk.
     int used = 0;
-    std::vector<int> nbk(nlev);
+    std::vector<int> nbk(nlev), chk(nlev);
     std::vector<int64_t> nch(nlev);
     int64_t ptot = 0;
     for (int l = 0; l < nlev; ++l) {
         int64_t tiles = (levels[l].n + NT - 1) / NT;
-        nch[l] = (tiles + CH - 1) / CH;
+        chk[l] = cg_chunk_tiles(levels[l].n);
+        nch[l] = (tiles + chk[l] - 1) / chk[l];
         if (nch[l] < 1) nch[l] = 1;
         ptot += 3 * nch[l];
         int want = levels[l].nblocks > 0
@@ -305,13 +478,14 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
         B.lev[l] = levels[l];
         B.lev[l].nblocks = nbk[l];
         B.lev[l].block_begin = begin;
+        B.lev[l].chunk_tiles = chk[l];
         B.lev[l].partials = partials + poff;
         B.lev[l].barrier = bars + l;
         begin += nbk[l];
         poff += 3 * nch[l];
     }
     void *args[] = {&B};
-    MSK_CUDA(cudaLaunchCooperativeKernel((void *)k_cg, dim3(used), dim3(NT), args, 0, st));
+    MSK_CUDA(cudaLaunchCooperativeKernel((void *)k_cg, dim3(used), dim3(NT), args, sizeof(CGShared), st));
     if (launches) *launches += 1;
     MSK_CUDA(cudaFreeAsync(partials, st));
     MSK_CUDA(cudaFreeAsync(bars, st));
@@ -320,7 +494,8 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
 void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,
               const double *v, double *y, cudaStream_t st, int *launches) {
     if (n == 0) return;
-    k_spmv<<<ceil_div_u(n, NT), NT, 0, st>>>(n, row_ptr, col, val, v, y);
+    set_smem_attrs();
+    k_spmv<<<ceil_div_u(n, NT), NT, sizeof(CGShared), st>>>(n, row_ptr, col, val, v, y);
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
 }

@@ -51,6 +51,7 @@ struct LevelView {
     double inv_delta;           // 1 / delta
     double scale;               // delta^-d
     const double *coef;         // coefficient vector (spatial order) for gathers
+    const double4 *rec;         // packed (x, y, z, coef) records (2-D: (x, y, coef, 0)) for gathers
 };
 
 // squared distance, left to right, round-to-nearest, no FMA (reading C-4)

@@ -54,6 +54,9 @@ struct GatherArgs {
     unsigned long long *hits;
 };
 void gather(const GatherArgs &a, cudaStream_t st, int *launches);
+// rec[i] = (x, y, z, coef) (2-D: (x, y, coef, 0)) from SoA xs (d arrays of n)
+void pack_records(int64_t n, int d, const double *xs, const double *coef, double4 *rec,
+                  cudaStream_t st, int *launches);
 
 // ---- cg.cu  (a4 / a8 block-diagonal CG, fused SpMV + reductions)
 struct CGLevelArgs {
@@ -72,6 +75,7 @@ struct CGLevelArgs {
     int max_iter;
     int nblocks;              // CTAs for this level (filled by launcher)
     int block_begin;
+    int chunk_tiles;          // tiles per reduction chunk (filled by launcher, function of n)
     double *partials;         // 3 * nblocks doubles (filled by launcher)
     unsigned long long *barrier;
     int *out_iters;           // device
@@ -79,6 +83,8 @@ struct CGLevelArgs {
     int *out_status;          // device: 0 ok, 1 noconv
 };
 // Run independent CGs on several levels in one cooperative launch.
+// CSR arrays must be 16-byte aligned and padded: row_ptr n+3 entries,
+// col nnz+4, val nnz+2 (bulk copies round their extents to 16 bytes).
 int cg_max_resident_blocks();
 void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches);
 void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,
