@@ -46,6 +46,8 @@ struct LevelData {
     double *val = nullptr;
     double *alpha = nullptr;       // coefficients of the last solve, spatial order
     double4 *rec = nullptr;        // packed (coords, coefficient) records for gathers
+    float4 *frec = nullptr;        // FP32 coordinates relative to lo (gather prefilter)
+    float fthr = 0.f;              // prefilter threshold
 };
 
 thread_local std::string g_err;
@@ -193,6 +195,8 @@ struct msk_hierarchy {
         v.scale = pow(D.delta, -(double)d);
         v.coef = coef;
         v.rec = D.rec;
+        v.frec = D.frec;
+        v.fthr = D.fthr;
         return v;
     }
 
@@ -217,7 +221,7 @@ struct msk_hierarchy {
         for (int l = 0; l < L; ++l) {
             LevelData &D = lev[l];
             dfree(D.xs, s); dfree(D.perm, s); dfree(D.cell_start, s); dfree(D.cnt, s);
-            dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s); dfree(D.rec, s);
+            dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s); dfree(D.rec, s); dfree(D.frec, s);
             D = LevelData();
         }
         dfree(ws, s);
@@ -347,6 +351,13 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
             co.cell_start = D.cell_start;
             co.keys = nullptr;
             build_cell_list(d, n[l], pts[l].ptr, D.g, true, co, st, &launches);
+            {  // FP32 prefilter coordinates (relative to lo) and threshold
+                double ext = 0.0;
+                for (int a = 0; a < d; ++a) ext = std::max(ext, h->hi[a] - h->lo[a]);
+                D.frec = dalloc<float4>((size_t)n[l], st);
+                pack_frecords(n[l], d, D.xs, h->lo, D.frec, st, &launches);
+                D.fthr = prefilter_threshold(delta[l], ext + delta[l], d);
+            }
             D.cnt = dalloc<int32_t>((size_t)n[l], st);
             minr2[l] = dalloc<unsigned long long>(1, st);
             unsigned long long inf = 0x7ff0000000000000ull;

@@ -52,6 +52,8 @@ struct LevelView {
     double scale;               // delta^-d
     const double *coef;         // coefficient vector (spatial order) for gathers
     const double4 *rec;         // packed (x, y, z, coef) records (2-D: (x, y, coef, 0)) for gathers
+    const float4 *frec;         // FP32 coordinates relative to g.lo (conservative prefilter)
+    float fthr;                 // prefilter threshold: r2_f >= fthr  =>  r^2 >= delta^2 for sure
 };
 
 // squared distance, left to right, round-to-nearest, no FMA (reading C-4)

@@ -18,6 +18,8 @@
 //   B products (eq:mas P:287): base = f^{(k)}, sign = -1, the
 //   levels l < k with c = t^{(l)} (reading C-7 for the sign).
 //   Evaluation (eq:fapproximation P:295): base = 0, sign = +1, all levels.
+#include <cmath>
+
 #include "kernels.cuh"
 #include "neighbors.cuh"
 
@@ -45,38 +47,52 @@ __global__ void __launch_bounds__(NT, 3) k_gather(GatherArgs a) {
     long long hits = 0;
     if (i < a.nt) {
         double x[3];
+        float xf[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-        for (int t = 0; t < D; ++t) x[t] = a.tx[t][i];
+        for (int t = 0; t < D; ++t) {
+            x[t] = a.tx[t][i];
+            xf[t] = (float)(x[t] - a.lev[0].g.lo[t]);  // same origin for every level
+        }
         double acc = 0.0;
         int hl[HMAX];
         for (int l = 0; l < a.nlev; ++l) {
             const LevelView &L = a.lev[l];
             const double d2 = L.delta2, inv = L.inv_delta;
             const double4 *__restrict__ rec = L.rec;
+            const float4 *__restrict__ frec = L.frec;
+            const float fthr = L.fthr;
             double s = 0.0;
             int nh = 0;
+            // exact FP64 test (reading C-4) + phi on the candidates that passed the prefilter
             auto flush = [&]() {
                 for (int h = 0; h < nh; ++h) {
                     const double4 R = rec[hl[h]];
                     const double r2 = rec_dist2<D>(x, R);
-                    s = fma(wendland<K>(sqrt(r2) * inv), rec_coef<D>(R), s);
+                    if (r2 < d2) {
+                        s = fma(wendland<K>(sqrt(r2) * inv), rec_coef<D>(R), s);
+                        ++hits;
+                    }
                 }
-                hits += nh;
                 nh = 0;
             };
             for_each_range<D>(L, x, [&](int b, int e) {
+                // conservative FP32 prefilter on 16-byte records; 2 candidates per trip
                 int j = b;
                 for (; j + 1 < e; j += 2) {
-                    const double4 R0 = rec[j], R1 = rec[j + 1];
-                    const bool h0 = rec_dist2<D>(x, R0) < d2, h1 = rec_dist2<D>(x, R1) < d2;
+                    const float4 F0 = frec[j], F1 = frec[j + 1];
+                    float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    float a1 = xf[0] - F1.x, b1 = xf[1] - F1.y, c1 = xf[2] - F1.z;
+                    const bool h0 = fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr;
+                    const bool h1 = fmaf(c1, c1, fmaf(b1, b1, a1 * a1)) < fthr;
                     if (nh + 2 > HMAX) flush();
                     if (h0) hl[nh++] = j;
                     if (h1) hl[nh++] = j + 1;
                 }
                 if (j < e) {
-                    const double4 R0 = rec[j];
+                    const float4 F0 = frec[j];
+                    float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
                     if (nh + 1 > HMAX) flush();
-                    if (rec_dist2<D>(x, R0) < d2) hl[nh++] = j;
+                    if (fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr) hl[nh++] = j;
                 }
             });
             flush();
@@ -99,7 +115,40 @@ __global__ void k_pack(int64_t n, int d, const double *__restrict__ x0, const do
     if (i >= n) return;
     rec[i] = d == 3 ? make_double4(x0[i], x1[i], x2[i], c[i]) : make_double4(x0[i], x1[i], c[i], 0.0);
 }
+
+__global__ void k_fpack(int64_t n, int d, const double *__restrict__ x0, const double *__restrict__ x1,
+                        const double *__restrict__ x2, double lo0, double lo1, double lo2,
+                        float4 *__restrict__ frec) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (i >= n) return;
+    frec[i] = make_float4((float)(x0[i] - lo0), (float)(x1[i] - lo1), d == 3 ? (float)(x2[i] - lo2) : 0.f, 0.f);
+}
 }  // namespace
+
+void pack_frecords(int64_t n, int d, const double *xs, const double *lo, float4 *frec, cudaStream_t st,
+                   int *launches) {
+    if (n == 0) return;
+    k_fpack<<<ceil_div_u(n, NT), NT, 0, st>>>(n, d, xs, xs + n, d == 3 ? xs + 2 * n : nullptr, lo[0], lo[1],
+                                             d == 3 ? lo[2] : 0.0, frec);
+    MSK_CHECK_LAUNCH();
+    if (launches) *launches += 1;
+}
+
+// Conservative FP32 prefilter threshold: with coordinates
+// stored as float(x - lo), |x - lo| <= M for every pair that can be within
+// delta, each float difference is off by at most e = 2^-24 (2M + delta) + tiny,
+// so a pair with r < delta has r_f <= delta + sqrt(d) e and, after the float
+// sum of squares, r2_f < (delta + sqrt(d) e)^2 (1 + 8 2^-24).  Any candidate
+// with r2_f >= that bound is outside the support for sure; the survivors get
+// the exact FP64 test.
+float prefilter_threshold(double delta, double M, int d) {
+    const double u = std::ldexp(1.0, -24);
+    const double e = u * (2.0 * M + delta) * (1.0 + 1e-6) + std::ldexp(1.0, -60);
+    const double t = (delta + std::sqrt((double)d) * e) * (delta + std::sqrt((double)d) * e) * (1.0 + 8.0 * u);
+    float f = (float)t;
+    if ((double)f < t) f = std::nextafter(f, INFINITY);
+    return std::nextafter(f, INFINITY);
+}
 
 void gather(const GatherArgs &a, cudaStream_t st, int *launches) {
     if (a.nt == 0) return;

@@ -57,6 +57,10 @@ void gather(const GatherArgs &a, cudaStream_t st, int *launches);
 // rec[i] = (x, y, z, coef) (2-D: (x, y, coef, 0)) from SoA xs (d arrays of n)
 void pack_records(int64_t n, int d, const double *xs, const double *coef, double4 *rec,
                   cudaStream_t st, int *launches);
+// frec[i] = float(x - lo) per axis (prefilter coordinates)
+void pack_frecords(int64_t n, int d, const double *xs, const double *lo, float4 *frec, cudaStream_t st,
+                   int *launches);
+float prefilter_threshold(double delta, double M, int d);
 
 // ---- cg.cu  (a4 / a8 block-diagonal CG, fused SpMV + reductions)
 struct CGLevelArgs {

@@ -190,7 +190,14 @@ def test_solve_matches_oracle(msk, ctx, name, schedule):
     assert np.all(np.abs(s - so) <= 1e-14 * scale + 1e-300)
     s_or = oracle.evaluate(H.points, H.delta, a_or, x, k=H.k)
     assert _rel(s, s_or) < BAR
-    assert einfo.nnz > 0
+    # hit counts of the matrix-free kernels == exact pattern sizes (the FP32
+    # prefilter never drops a pair inside the support)
+    ev_nnz = sum(int(oracle.pattern(x, P, dl)[0][-1]) for P, dl in zip(H.points, H.delta))
+    assert einfo.nnz == ev_nnz
+    b_nnz = sum(int(oracle.pattern(H.points[k], H.points[l], H.delta[l])[0][-1])
+                for k in range(H.L) for l in range(k))
+    sweeps = H.L if schedule == "literal" else 1
+    assert info.nnz_gather == sweeps * b_nnz
 
 
 def test_pruned_equals_literal(msk, ctx):
