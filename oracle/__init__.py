@@ -79,6 +79,9 @@ def lib():
         L.mo_jacobi_literal.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, pp, _dp,
                                         pp, pp, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                         ctypes.c_int64, pp, pp]
+        L.mo_thresholded.restype = ctypes.c_int
+        L.mo_thresholded.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, pp, _dp, _dp,
+                                     ctypes.c_double, pp, pp, pp, _i64p]
         L.mo_separation.restype = ctypes.c_double
         L.mo_separation.argtypes = [ctypes.c_int, ctypes.c_int64, _dp]
         L.mo_mas_row_residual.restype = ctypes.c_double
@@ -241,6 +244,25 @@ def jacobi_literal(points, delta, f, tol=1e-12, inner_tol=None, beta0=None, k=1,
     if st:
         raise RuntimeError(f"oracle jacobi failed ({st})")
     return alpha, beta
+
+
+def thresholded(points, delta, q, T, f, k=1):
+    """O7: forward substitution with M~(T) + block solves. Returns (alpha, beta, nnz)."""
+    pts, d, n, dl = _hier_args(points, delta)
+    qq = _c(q)
+    fs = [_c(x) for x in f]
+    alpha = [np.zeros(int(m)) for m in n]
+    beta = [np.zeros(int(m)) for m in n]
+    pp, _k1 = _ptrs(pts)
+    fp, _k2 = _ptrs(fs)
+    ap, _k3 = _ptrs(alpha)
+    bp, _k4 = _ptrs(beta)
+    nnz = np.zeros(1, dtype=np.int64)
+    st = lib().mo_thresholded(d, k, len(pts), _ptr(n, _i64p), pp, _ptr(dl), _ptr(qq), float(T), fp, bp, ap,
+                              _ptr(nnz, _i64p))
+    if st:
+        raise RuntimeError(f"oracle thresholded solve failed ({st})")
+    return alpha, beta, int(nnz[0])
 
 
 def separation(P):

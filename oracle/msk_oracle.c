@@ -495,6 +495,67 @@ int mo_jacobi_literal(int d, int k, int L, const int64_t *n, const double *const
 }
 
 /* ------------------------------------------------------------------------- */
+/* O7  Thresholded factor and its forward substitution                        */
+/* ------------------------------------------------------------------------- */
+
+/* (id - M~(T)) beta = f with M~ = -X~ blocks (eq:perturbedmatrix P:846-861,
+ * eq:perturbed_split P:865-869; reading C-7 for the sign), solved by forward
+ * substitution in level order (the Jacobi iteration reaches the same vector
+ * after L sweeps, Theorem jacobi):
+ *   beta^(1) = f^(1);
+ *   beta^(k) = f^(k) - sum_{l<k} sum_i X~_kl[j,i] beta_i^(l),
+ * where X~_kl[j,i] = chi_i^(l)(x_j^(k)) if ||x_j^(k) - x_i^(l)||^2 < (T q_l)^2
+ * (strict, coarse column level's q, reading C-5) and the Lagrange function
+ * chi_i^(l) = sum_h c_i[h] Phi_l(. - x_h^(l)), c_i = A_l^{-1} e_i (eq:chi
+ * P:373-377), by dense Cholesky (A_l SPD).  Then alpha^(l) =
+ * A_l^{-1} beta^(l) (eq:blockdiagonal_levelwise P:616), also by Cholesky.
+ * Columns are processed in level order, so every beta^(l) used is final.
+ * nnz_out (nullable): number of stored factor entries.  Intended for small
+ * coarse levels (dense O(N(l)^3)). */
+int mo_thresholded(int d, int k, int L, const int64_t *n, const double *const *pts,
+                   const double *delta, const double *q, double T, const double *const *f,
+                   double *const *beta, double *const *alpha, int64_t *nnz_out)
+{
+    int64_t nnz = 0;
+    for (int l = 0; l < L; ++l) memcpy(beta[l], f[l], sizeof(double) * (size_t)n[l]);
+    double *e = NULL, *c = NULL;
+    for (int l = 0; l + 1 < L; ++l) {
+        mo_csr A;
+        if (build_A(d, k, n[l], pts[l], delta[l], &A)) return -1;
+        e = (double *)realloc(e, sizeof(double) * (size_t)n[l]);
+        c = (double *)realloc(c, sizeof(double) * (size_t)n[l]);
+        const double R = T * q[l], R2 = R * R;
+        for (int64_t i = 0; i < n[l]; ++i) {
+            for (int64_t h = 0; h < n[l]; ++h) e[h] = 0.0;
+            e[i] = 1.0;
+            if (mo_cholesky_solve(A.n, A.row_ptr, A.col, A.val, e, c)) { csr_free(&A); return 2; }
+            for (int kk = l + 1; kk < L; ++kk)
+                for (int64_t j = 0; j < n[kk]; ++j) {
+                    const double *xj = pts[kk] + j * d;
+                    if (!(dist2(d, xj, pts[l] + i * d) < R2)) continue;
+                    double chi = 0.0;
+                    for (int64_t h = 0; h < n[l]; ++h)
+                        chi += c[h] * mo_kernel(d, k, delta[l], xj, pts[l] + h * d);
+                    beta[kk][j] -= chi * beta[l][i];
+                    ++nnz;
+                }
+        }
+        csr_free(&A);
+    }
+    free(e);
+    free(c);
+    for (int l = 0; l < L; ++l) {
+        mo_csr A;
+        if (build_A(d, k, n[l], pts[l], delta[l], &A)) return -1;
+        int st = mo_cholesky_solve(A.n, A.row_ptr, A.col, A.val, beta[l], alpha[l]);
+        csr_free(&A);
+        if (st) return 2;
+    }
+    if (nnz_out) *nnz_out = nnz;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* Geometry                                                                   */
 /* ------------------------------------------------------------------------- */
 

@@ -8,9 +8,11 @@
 * Theorem decayerror property: the error shrinks as T grows (overall)
 """
 import numpy as np
+import pytest
 
+import oracle
 from oracle import dense
-from workloads import grid_hierarchy
+from workloads import grid_hierarchy, halton_hierarchy
 
 
 def test_infinite_T_equals_exact():
@@ -35,6 +37,38 @@ def test_lagrange_property_nested_grid():
             e = np.zeros(Pb.shape[0])
             e[i] = 1.0
             assert np.abs(blk[j] - e).max() < 1e-10
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.mark.parametrize("L", [3, 4])
+@pytest.mark.parametrize("T", [1.0, 2.5, 4.0])
+def test_c_oracle_equals_dense_thresholded(L, T):
+    """The C oracle's forward substitution with M~(T) (O7) equals the dense
+    numpy form (Jacobi on the dense masked M, itself pinned by Figures 2-3),
+    and its entry count equals the geometric mask size."""
+    H = grid_hierarchy(L)
+    f = H.f()
+    Xi = dense.Xi_blocks(H.points, H.delta)
+    a_d, b_d = dense.thresholded_solve(H.points, H.delta, H.q, f, T, Xi=Xi)
+    a_c, b_c, nnz = oracle.thresholded(H.points, H.delta, H.q, T, f)
+    mask = dense.truncation_mask(H.points, H.q, T)
+    assert nnz == sum(int(m.sum()) for m in mask.values())
+    for l in range(H.L):
+        assert _rel(b_c[l], b_d[l]) < 1e-11
+        assert _rel(a_c[l], a_d[l]) < 1e-10
+
+
+def test_c_oracle_thresholded_large_T_is_exact():
+    H = halton_hierarchy("t", 3, [40, 320, 1200], 1.5)
+    f = H.f()
+    a_t, _, _ = oracle.thresholded(H.points, H.delta, H.q, 1e6, f)
+    a_s, _, _ = oracle.sequential(H.points, H.delta, f, direct_max_n=10 ** 6)
+    for l in range(H.L):
+        assert _rel(a_t[l], a_s[l]) < 1e-10
 
 
 def test_pert1_bound_and_decay():
