@@ -153,11 +153,19 @@ MSK_API void msk_hierarchy_destroy(msk_hierarchy *h);
 /* Facts about the hierarchy (sizes, nnz, timings of the last create/assemble). */
 MSK_API msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_info *info);
 
-/* a2 (+ a6 later): assemble the level matrices A_l in CSR (pattern r^2 <
- * delta_l^2, strict, bit-exact; values Phi_{delta_l}).  T <= 0: exact mode
- * (B_{kl} stay matrix-free).  T > 0 (thresholded factor M~(T), eq:
- * perturbedmatrix P:846-861) is not available in this version and returns
- * MSK_ERR_INVALID.  lagrange_tol is reserved for T > 0. */
+/* a2 (+ a6): assemble the level matrices A_l in CSR (pattern r^2 <
+ * delta_l^2, strict, bit-exact; values Phi_{delta_l}).
+ *   T <= 0: exact mode; the B_{kl} stay matrix-free and msk_solve runs the
+ *           exact Jacobi of Algorithm 2 (inner CG solves).
+ *   T > 0:  additionally build the thresholded factor M~(T) (eq:perturbedmatrix
+ *           P:846-861): X~_{kl}[j,i] = chi_i^{(l)}(x_j^{(k)}) kept iff
+ *           ||x_j^{(k)} - x_i^{(l)}||^2 < (T q_l)^2 (coarse level's q,
+ *           strict; reading C-5), with the Lagrange coefficients
+ *           A_l^{-1} e_i (eq:chi P:373-377) solved by CG to relative residual
+ *           lagrange_tol in (0,1).  msk_solve then runs the Jacobi sweep with
+ *           the stored factor (eq:perturbed_split P:865-869).  Cost grows
+ *           like sum_l N(l)^2 (one solve per coarse column).
+ * Non-convergence of a Lagrange solve => MSK_ERR_NOCONV. */
 MSK_API msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol);
 
 /* a3-a5, a8: solve T_L alpha = f (eq:bigt) through eq:split.
@@ -193,6 +201,14 @@ MSK_API msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x,
  * bit-exact (reading C-4). */
 MSK_API msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_level, int64_t *row_ptr,
                             int32_t *col, double *val);
+
+/* Entries of the thresholded factor block X~_{row_level,col_level}(T)
+ * (eq:perturbedmatrix P:846-861; 0 <= col_level < row_level) built by the last
+ * msk_assemble(T > 0), in CALLER indices with ascending columns: row_ptr
+ * [host] n[row_level]+1, col / val [host] nnz or NULL (query), T_out
+ * (nullable) the T it was built for.  MSK_ERR_STATE without a factor. */
+MSK_API msk_status msk_export_factor(msk_hierarchy *h, int row_level, int col_level, int64_t *row_ptr,
+                                     int32_t *col, double *val, double *T_out);
 
 /* Cell list of level l [host outputs]: perm (n[l] int32, sorted position ->
  * caller index), cell_start (ncells+1 int32), cell_key (n[l] int64, key of

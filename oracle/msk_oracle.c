@@ -313,17 +313,18 @@ int mo_cg(int64_t n, const int64_t *row_ptr, const int32_t *col,
 
 /* Direct solve of A x = b via dense Cholesky A = L L^T (A SPD).
  * Returns 0, or 2 if A is not numerically positive definite. */
-int mo_cholesky_solve(int64_t n, const int64_t *row_ptr, const int32_t *col,
-                      const double *val, const double *b, double *x)
+/* dense lower Cholesky factor of CSR A (n x n), or NULL (not SPD / no memory) */
+static double *chol_factor(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                           const double *val, int *status)
 {
-    double *A = (double *)calloc((size_t)(n * n), sizeof(double));
-    if (!A) return -1;
+    double *A = (double *)calloc((size_t)(n * n > 0 ? n * n : 1), sizeof(double));
+    if (!A) { *status = -1; return NULL; }
     for (int64_t i = 0; i < n; ++i)
         for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) A[i * n + col[p]] = val[p];
     for (int64_t j = 0; j < n; ++j) {
         double s = A[j * n + j];
         for (int64_t t = 0; t < j; ++t) s -= A[j * n + t] * A[j * n + t];
-        if (!(s > 0.0)) { free(A); return 2; }
+        if (!(s > 0.0)) { free(A); *status = 2; return NULL; }
         double ljj = sqrt(s);
         A[j * n + j] = ljj;
         for (int64_t i = j + 1; i < n; ++i) {
@@ -332,6 +333,13 @@ int mo_cholesky_solve(int64_t n, const int64_t *row_ptr, const int32_t *col,
             A[i * n + j] = u / ljj;
         }
     }
+    *status = 0;
+    return A;
+}
+
+/* x = (L L^T)^{-1} b with the factor of chol_factor */
+static void chol_solve(int64_t n, const double *A, const double *b, double *x)
+{
     for (int64_t i = 0; i < n; ++i) {            /* L y = b */
         double s = b[i];
         for (int64_t t = 0; t < i; ++t) s -= A[i * n + t] * x[t];
@@ -342,6 +350,15 @@ int mo_cholesky_solve(int64_t n, const int64_t *row_ptr, const int32_t *col,
         for (int64_t t = i + 1; t < n; ++t) s -= A[t * n + i] * x[t];
         x[i] = s / A[i * n + i];
     }
+}
+
+int mo_cholesky_solve(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                      const double *val, const double *b, double *x)
+{
+    int st = 0;
+    double *A = chol_factor(n, row_ptr, col, val, &st);
+    if (!A) return st;
+    chol_solve(n, A, b, x);
     free(A);
     return 0;
 }
@@ -525,10 +542,13 @@ int mo_thresholded(int d, int k, int L, const int64_t *n, const double *const *p
         e = (double *)realloc(e, sizeof(double) * (size_t)n[l]);
         c = (double *)realloc(c, sizeof(double) * (size_t)n[l]);
         const double R = T * q[l], R2 = R * R;
+        int st = 0;
+        double *F = chol_factor(A.n, A.row_ptr, A.col, A.val, &st);
+        if (!F) { csr_free(&A); return st; }
         for (int64_t i = 0; i < n[l]; ++i) {
             for (int64_t h = 0; h < n[l]; ++h) e[h] = 0.0;
             e[i] = 1.0;
-            if (mo_cholesky_solve(A.n, A.row_ptr, A.col, A.val, e, c)) { csr_free(&A); return 2; }
+            chol_solve(A.n, F, e, c);
             for (int kk = l + 1; kk < L; ++kk)
                 for (int64_t j = 0; j < n[kk]; ++j) {
                     const double *xj = pts[kk] + j * d;
@@ -540,6 +560,7 @@ int mo_thresholded(int d, int k, int L, const int64_t *n, const double *const *p
                     ++nnz;
                 }
         }
+        free(F);
         csr_free(&A);
     }
     free(e);

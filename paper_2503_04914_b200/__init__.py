@@ -125,6 +125,13 @@ def msk_export_block(h, row_level, col_level, row_ptr, col, val):
     check(load().msk_export_block(h, row_level, col_level, _ptr(row_ptr), _ptr(col), _ptr(val)))
 
 
+def msk_export_factor(h, row_level, col_level, row_ptr, col, val):
+    T = ctypes.c_double(0.0)
+    check(load().msk_export_factor(h, row_level, col_level, _ptr(row_ptr), _ptr(col), _ptr(val),
+                                   ctypes.byref(T)))
+    return T.value
+
+
 def msk_export_cells(h, level, perm, cell_start, cell_key, lo, cell, dims):
     check(load().msk_export_cells(h, level, _ptr(perm), _ptr(cell_start), _ptr(cell_key), _ptr(lo),
                                   _ptr(cell), _ptr(dims)))
@@ -235,6 +242,17 @@ class Hierarchy:
         val = np.zeros(max(nnz, 1), dtype=np.float64)
         msk_export_block(self.handle, row_level, col_level, rp, col, val)
         return rp, col[:nnz], val[:nnz]
+
+    def export_factor(self, row_level: int, col_level: int):
+        """Entries of X~_{row_level,col_level}(T) (caller indices, CSR)."""
+        n = self.n[row_level]
+        rp = np.zeros(n + 1, dtype=np.int64)
+        msk_export_factor(self.handle, row_level, col_level, rp, None, None)
+        nnz = int(rp[-1])
+        col = np.zeros(max(nnz, 1), dtype=np.int32)
+        val = np.zeros(max(nnz, 1), dtype=np.float64)
+        T = msk_export_factor(self.handle, row_level, col_level, rp, col, val)
+        return rp, col[:nnz], val[:nnz], T
 
     def export_cells(self, level: int):
         info = self.info()

@@ -80,6 +80,8 @@ def load() -> ctypes.CDLL:
         "msk_evaluate_ex": ([_vp, _i64, _vp, _vp, ctypes.POINTER(EvalInfo)], ctypes.c_int),
         "msk_export_block": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
         "msk_export_cells": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+        "msk_export_factor": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(_dbl)],
+                              ctypes.c_int),
         "msk_apply_block": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.POINTER(_dbl)], ctypes.c_int),
         "msk_cg_level": ([_vp, ctypes.c_int, _vp, _vp, _dbl, _i32, ctypes.POINTER(_i32),
                           ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)], ctypes.c_int),
@@ -96,7 +98,7 @@ def load() -> ctypes.CDLL:
 
 EXPORTED = ["msk_ctx_create", "msk_ctx_destroy", "msk_hierarchy_create", "msk_hierarchy_destroy",
             "msk_hierarchy_info_get", "msk_assemble", "msk_solve", "msk_evaluate", "msk_evaluate_ex",
-            "msk_export_block", "msk_export_cells", "msk_apply_block", "msk_cg_level",
+            "msk_export_block", "msk_export_factor", "msk_export_cells", "msk_apply_block", "msk_cg_level",
             "msk_last_error", "msk_version"]
 
 

@@ -180,6 +180,23 @@ struct msk_hierarchy {
     double *ws = nullptr;  // CG workspace: r, p, q, beta, t (5 * ntot)
     double t_create_ms = 0, t_assemble_ms = 0;
     int launches_create = 0, launches_assemble = 0;
+    // thresholded factor M~(T) (a6): one CSR over all points (rows of level 1
+    // are empty), global level-major spatial column indices
+    double T = 0.0;
+    int64_t tnnz = 0;
+    int64_t *trow_ptr = nullptr;
+    int32_t *tcol = nullptr;
+    double *tval = nullptr;
+    int lagrange_max_iters = 0;
+    double t_lagrange_ms = 0;
+
+    void release_factor() {
+        cudaStream_t s = st();
+        dfree(trow_ptr, s); dfree(tcol, s); dfree(tval, s);
+        trow_ptr = nullptr; tcol = nullptr; tval = nullptr;
+        tnnz = 0;
+        T = 0.0;
+    }
 
     cudaStream_t st() const { return ctx->stream; }
 
@@ -226,6 +243,7 @@ struct msk_hierarchy {
         }
         dfree(ws, s);
         ws = nullptr;
+        release_factor();
     }
 };
 
@@ -423,13 +441,136 @@ extern "C" msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarc
 }
 
 // ================================================================ assemble
+namespace {
+
+// a6: the thresholded factor X~_{kl}(T) of all blocks k > l (eq:perturbedmatrix
+// P:846-861): geometric pattern ||x_j^(k) - x_i^(l)||^2 < (T q_l)^2 (reading
+// C-5), values chi_i^(l)(x_j^(k)) from Lagrange columns c_i = A_l^{-1} e_i
+// solved by the multi-RHS CG at lagrange_tol (eq:chi P:373-377).
+void build_factor(msk_hierarchy *h, double T, double lagrange_tol, int *launches) {
+    cudaStream_t st = h->st();
+    const int L = h->L, d = h->d;
+    const int64_t ntot = h->ntot;
+    // ---- pattern: rows = all points (level 0 rows empty), columns global
+    int32_t *cnt = dalloc<int32_t>((size_t)ntot, st);
+    MSK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)ntot, st));
+    auto pattern_args = [&](int k) {
+        ThreshPatternArgs a{};
+        a.d = d;
+        a.nt = h->lev[k].n;
+        for (int q = 0; q < d; ++q) a.tx[q] = h->lev[k].xs + (size_t)q * h->lev[k].n;
+        a.nlev = k;
+        for (int l = 0; l < k; ++l) {
+            a.lev[l] = h->view(l);
+            const double R = T * h->lev[l].q;
+            a.R2[l] = R * R;
+            a.reach[l] = (int)std::min(floor(R * h->lev[l].g.inv_cell) + 1.0, 1e6);
+            a.col_off[l] = h->off[l];
+        }
+        return a;
+    };
+    for (int k = 1; k < L; ++k) {
+        ThreshPatternArgs a = pattern_args(k);
+        a.cnt = cnt + h->off[k];
+        thresh_count(a, st, launches);
+    }
+    h->trow_ptr = dalloc<int64_t>((size_t)(ntot + 1), st);
+    exclusive_scan_i64(cnt, ntot, h->trow_ptr, st, launches);
+    int64_t nnz = 0;
+    MSK_CUDA(cudaMemcpyAsync(&nnz, h->trow_ptr + ntot, sizeof nnz, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(cnt, st);
+    h->tnnz = nnz;
+    h->tcol = dalloc<int32_t>((size_t)nnz, st);
+    h->tval = dalloc<double>((size_t)nnz, st);
+    for (int k = 1; k < L; ++k) {
+        ThreshPatternArgs a = pattern_args(k);
+        a.row_ptr = h->trow_ptr + h->off[k];
+        a.col = h->tcol;
+        thresh_fill(a, st, launches);
+    }
+    // ---- transpose index over the coarse columns (levels 0..L-2)
+    const int64_t ncols = h->off[L - 1];
+    int64_t *cptr = dalloc<int64_t>((size_t)(ncols + 1), st);
+    int64_t *cpos = dalloc<int64_t>((size_t)nnz, st);
+    int32_t *crow = dalloc<int32_t>((size_t)nnz, st);
+    int32_t *ccol = dalloc<int32_t>((size_t)nnz, st);
+    thresh_csc(ntot - h->off[1], h->off[1], nnz, ncols, h->trow_ptr, h->tcol, cptr, cpos, crow, ccol, st,
+               launches);
+    std::vector<int64_t> hcptr((size_t)(ncols + 1));
+    MSK_CUDA(cudaMemcpyAsync(hcptr.data(), cptr, sizeof(int64_t) * (ncols + 1), cudaMemcpyDeviceToHost, st));
+    int *dstat = dalloc<int>(2, st);
+    MSK_CUDA(cudaMemsetAsync(dstat, 0, 2 * sizeof(int), st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    // ---- Lagrange columns, level by level, rounds of concurrent 32-column batches
+    const int resident = 4 * 148;
+    const double budget = 8e9;  // bytes of CG workspace per round
+    for (int l = 0; l + 1 < L; ++l) {
+        const LevelData &D = h->lev[l];
+        const int64_t nb_total = (D.n + 31) / 32;
+        const double slot_bytes = 4.0 * (double)D.n * 32.0 * 8.0;
+        int64_t slots = std::min<int64_t>(nb_total, std::max<int64_t>(1, std::min<int64_t>(resident, (int64_t)(budget / slot_bytes))));
+        double *ws = dalloc<double>((size_t)(slots * 4 * D.n * 32), st);
+        for (int64_t b0 = 0; b0 < nb_total; b0 += slots) {
+            const int64_t nb = std::min<int64_t>(slots, nb_total - b0);
+            CGMultiArgs m{};
+            m.n = D.n;
+            m.ncols = D.n;
+            m.row_ptr = D.row_ptr;
+            m.col = D.col;
+            m.val = D.val;
+            m.tol2 = lagrange_tol * lagrange_tol;
+            m.max_iter = 20000;
+            m.batch0 = b0;
+            m.nbatches = nb_total;
+            m.ws = ws;
+            m.fail = dstat;
+            m.max_iters = dstat + 1;
+            thresh_cg_multi(m, (int)nb, st, launches);
+            const int64_t c0 = b0 * 32, c1 = std::min<int64_t>((b0 + nb) * 32, D.n);
+            ThreshValueArgs v{};
+            v.d = d;
+            v.k = h->k;
+            v.L = L;
+            v.pos0 = hcptr[h->off[l] + c0];
+            v.pos1 = hcptr[h->off[l] + c1];
+            v.cpos = cpos;
+            v.crow = crow;
+            v.ccol = ccol;
+            v.col_off = (int32_t)h->off[l];
+            v.first_col = c0;
+            for (int q = 0; q <= L; ++q) v.lev_off[q] = h->off[q];
+            for (int q = 0; q < L; ++q) {
+                v.lev_xs[q] = h->lev[q].xs;
+                v.lev_n[q] = h->lev[q].n;
+            }
+            v.Lv = h->view(l);
+            v.ws = ws;
+            v.val = h->tval;
+            thresh_values(v, st, launches);
+        }
+        dfree(ws, st);
+    }
+    int hstat[2];
+    MSK_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof hstat, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(dstat, st); dfree(cptr, st); dfree(cpos, st); dfree(crow, st); dfree(ccol, st);
+    h->lagrange_max_iters = hstat[1];
+    h->T = T;
+    if (hstat[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: Lagrange CG did not converge in 20000 iterations");
+}
+
+}  // namespace
+
 extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol) {
     API_BEGIN
     require(h != nullptr, "msk_assemble: NULL hierarchy");
-    require(!(T > 0.0), "msk_assemble: the thresholded factor (T > 0) is not available in this version");
-    (void)lagrange_tol;
+    require(std::isfinite(T), "msk_assemble: T must be finite");
+    require(!(T > 0.0) || (lagrange_tol > 0.0 && lagrange_tol < 1.0),
+            "msk_assemble: lagrange_tol must be in (0,1) when T > 0");
     MSK_CUDA(cudaSetDevice(h->ctx->device));
     cudaStream_t st = h->st();
+    h->release_factor();
     Timer tm(st);
     tm.start();
     int launches = 0;
@@ -453,6 +594,7 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
         LevelView v = h->view(l);
         fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
     }
+    if (T > 0.0 && h->L > 1) build_factor(h, T, lagrange_tol, &launches);
     tm.stop();
     MSK_CUDA(cudaStreamSynchronize(st));
     h->t_assemble_ms = tm.ms();
@@ -583,7 +725,44 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         alpha_sp[l] = h->lev[l].alpha;
         t_sp[l] = h->ws_t(l);
     }
-    if (schedule == MSK_SCHED_PRUNED) {
+    const bool thresholded = h->T > 0.0;
+    if (thresholded) {
+        // a7: Jacobi on (id - M~(T)) beta = f (eq:perturbed_split P:865-869),
+        // beta^(k) = f^(k) - sum_{l<k} X~_kl beta^(l) with the stored factor;
+        // PRUNED = forward substitution (each block row once, in level order),
+        // LITERAL = L full sweeps from beta_0 = f.  Then D_L alpha = beta by the
+        // block-diagonal CG on ALL levels in one batched launch (Algorithm 1).
+        double *fsp = h->ws_r(0);
+        for (int l = 0; l < L; ++l)
+            permute_gather(h->lev[l].n, fd[l].ptr, h->lev[l].perm, fsp + h->off[l], st, &launches);
+        double *beta = h->ws_beta(0);
+        if (schedule == MSK_SCHED_PRUNED) {
+            MSK_CUDA(cudaMemcpyAsync(beta, fsp, sizeof(double) * h->ntot, cudaMemcpyDeviceToDevice, st));
+            time_ga();
+            for (int k = 1; k < L; ++k)
+                thresh_residual(h->off[k], h->off[k + 1], h->trow_ptr, h->tcol, h->tval, beta, beta, beta, st,
+                                &launches);
+            ga_t.back()->stop();
+        } else {
+            double *cur = h->ws_beta(0), *nxt = h->ws_t(0);
+            MSK_CUDA(cudaMemcpyAsync(cur, fsp, sizeof(double) * h->ntot, cudaMemcpyDeviceToDevice, st));
+            MSK_CUDA(cudaMemcpyAsync(nxt, fsp, sizeof(double) * h->ntot, cudaMemcpyDeviceToDevice, st));
+            time_ga();
+            for (int sweep = 0; sweep < L; ++sweep) {
+                thresh_residual(h->off[1], h->ntot, h->trow_ptr, h->tcol, h->tval, fsp, cur, nxt, st, &launches);
+                std::swap(cur, nxt);
+            }
+            ga_t.back()->stop();
+            beta = cur;
+        }
+        std::vector<CGLevelArgs> a;
+        for (int l = 0; l < L; ++l)
+            a.push_back(cg_args(h, l, tol, max_iter, beta + h->off[l], nullptr, alpha_sp[l], ad[l].ptr,
+                                d_it + l, d_rr + 2 * l, d_stat + l));
+        time_cg(-1);
+        cg_batched(a.data(), L, st, &launches);
+        cg_t.back()->stop();
+    } else if (schedule == MSK_SCHED_PRUNED) {
         // Algorithm 2 with every inner solve done once, when its input is final:
         // beta^(l) = f^(l) - sum_{k<l} B_lk t^(k); t^(l) = A_l^{-1} beta^(l);
         // alpha^(l) = t^(l) (the final block CG of a converged block is the
@@ -647,12 +826,13 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     memset(&loc, 0, sizeof loc);
     loc.L = L;
     loc.jacobi_sweeps = schedule == MSK_SCHED_LITERAL ? L : 0;
-    const int fin = schedule == MSK_SCHED_LITERAL ? L : 0;  // slot of the final solves
+    const int fin = schedule == MSK_SCHED_LITERAL && !thresholded ? L : 0;  // slot of the final solves
+    if (thresholded) hits = (unsigned long long)(h->tnnz * (schedule == MSK_SCHED_LITERAL ? L : 1));
     std::string noconv;
-    for (int s = 0; s < nslots; ++s)
+    for (int s = 0; s < (thresholded ? 1 : nslots); ++s)
         for (int l = 0; l < L; ++l) {
             int idx = s * L + l;
-            bool used = schedule == MSK_SCHED_PRUNED || s == fin || l + 1 < L;
+            bool used = thresholded || schedule == MSK_SCHED_PRUNED || s == fin || l + 1 < L;
             if (!used) continue;
             if (stat[idx] && noconv.empty()) {
                 char buf[160];
@@ -822,6 +1002,53 @@ extern "C" msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_
         }
     }
     row_ptr[nr] = pos;
+    API_END
+}
+
+extern "C" msk_status msk_export_factor(msk_hierarchy *h, int row_level, int col_level, int64_t *row_ptr,
+                                        int32_t *col, double *val, double *T_out) {
+    API_BEGIN
+    require(h && row_ptr, "msk_export_factor: NULL argument");
+    require(row_level >= 0 && row_level < h->L && col_level >= 0 && col_level < row_level,
+            "msk_export_factor: need 0 <= col_level < row_level < L");
+    if (!(h->T > 0.0)) throw Error(MSK_ERR_STATE, "msk_export_factor: no thresholded factor (msk_assemble with T > 0)");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const LevelData &R = h->lev[row_level], &C = h->lev[col_level];
+    const int64_t r0 = h->off[row_level], nr = R.n;
+    std::vector<int64_t> hrp((size_t)(nr + 1));
+    MSK_CUDA(cudaMemcpyAsync(hrp.data(), h->trow_ptr + r0, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    const int64_t p0 = hrp[0], np = hrp[nr] - hrp[0];
+    std::vector<int32_t> hcl((size_t)np), rperm((size_t)nr), cperm((size_t)C.n);
+    std::vector<double> hvl((size_t)np);
+    if (np) {
+        MSK_CUDA(cudaMemcpyAsync(hcl.data(), h->tcol + p0, sizeof(int32_t) * np, cudaMemcpyDeviceToHost, st));
+        MSK_CUDA(cudaMemcpyAsync(hvl.data(), h->tval + p0, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    }
+    MSK_CUDA(cudaMemcpyAsync(rperm.data(), R.perm, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(cperm.data(), C.perm, sizeof(int32_t) * C.n, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> inv((size_t)nr);
+    for (int64_t i = 0; i < nr; ++i) inv[rperm[i]] = i;
+    const int64_t c_lo = h->off[col_level], c_hi = h->off[col_level + 1];
+    int64_t pos = 0;
+    std::vector<std::pair<int32_t, double>> tmp;
+    for (int64_t j = 0; j < nr; ++j) {
+        row_ptr[j] = pos;
+        const int64_t i = inv[j];
+        tmp.clear();
+        for (int64_t p = hrp[i] - p0; p < hrp[i + 1] - p0; ++p)
+            if (hcl[p] >= c_lo && hcl[p] < c_hi) tmp.emplace_back(cperm[hcl[p] - c_lo], hvl[p]);
+        std::sort(tmp.begin(), tmp.end());
+        for (auto &e : tmp) {
+            if (col) col[pos] = e.first;
+            if (val) val[pos] = e.second;
+            ++pos;
+        }
+    }
+    row_ptr[nr] = pos;
+    if (T_out) *T_out = h->T;
     API_END
 }
 

@@ -94,6 +94,60 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches);
 void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,
               const double *v, double *y, cudaStream_t st, int *launches);
 
+// ---- thresh.cu  (a6 / a7 thresholded factor)
+struct ThreshPatternArgs {
+    int d;
+    int64_t nt;                     // target rows (points of one finer level, spatial order)
+    const double *tx[3];
+    int nlev;                       // coarse levels 0..nlev-1
+    LevelView lev[kMaxLevels];
+    double R2[kMaxLevels];          // (T q_l)^2
+    int reach[kMaxLevels];          // cells per axis covering T q_l
+    int64_t col_off[kMaxLevels];    // global column offset of level l
+    const int64_t *row_ptr;         // fill: row pointers of these rows
+    int32_t *cnt;                   // count: output
+    int32_t *col;                   // fill: output (global columns)
+};
+void thresh_count(const ThreshPatternArgs &a, cudaStream_t st, int *launches);
+void thresh_fill(const ThreshPatternArgs &a, cudaStream_t st, int *launches);
+// transpose index of the factor pattern: for each coarse column c (global),
+// positions cpos[cptr[c]..cptr[c+1]) of its entries, their rows crow and ccol = c
+void thresh_csc(int64_t nrows_total, int64_t row0, int64_t nnz, int64_t ncols, const int64_t *row_ptr,
+                const int32_t *col, int64_t *cptr, int64_t *cpos, int32_t *crow, int32_t *ccol,
+                cudaStream_t st, int *launches);
+struct CGMultiArgs {
+    int64_t n, ncols;               // A_l size; columns to solve (= n)
+    const int64_t *row_ptr;
+    const int32_t *col;
+    const double *val;
+    double tol2;
+    int max_iter;
+    int64_t batch0, nbatches;       // batches (of 32 columns) of this launch start at batch0
+    double *ws;                     // per CTA: X, R, P, Q (n x 32 each, row-major)
+    int *fail;                      // device counter of batches that hit max_iter
+    int *max_iters;                 // device max of iterations
+};
+void thresh_cg_multi(const CGMultiArgs &a, int nblocks, cudaStream_t st, int *launches);
+struct ThreshValueArgs {
+    int d, k, L;
+    int64_t pos0, pos1;             // CSC positions of this round's columns
+    const int64_t *cpos;
+    const int32_t *crow;
+    const int32_t *ccol;
+    int32_t col_off;                // global column offset of the coarse level
+    int64_t first_col;              // first (level-local) column of this round
+    int64_t lev_off[kMaxLevels + 1];
+    const double *lev_xs[kMaxLevels];
+    int64_t lev_n[kMaxLevels];
+    LevelView Lv;                   // the coarse level
+    const double *ws;               // the round's CG workspaces (X first)
+    double *val;                    // factor values (output)
+};
+void thresh_values(const ThreshValueArgs &a, cudaStream_t st, int *launches);
+// out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)
+void thresh_residual(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col, const double *val,
+                     const double *base, const double *v, double *out, cudaStream_t st, int *launches);
+
 // ---- misc.cu
 // mm[0..2] = ordered keys of per-axis minima (init ~0), mm[3..5] maxima (init 0)
 void minmax_points(int64_t n, int d, const double *pts, unsigned long long *mm, cudaStream_t st,
