@@ -120,10 +120,11 @@ def run_msk(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     ctx = msk.Context(local_rank, stream.cuda_stream)
     sched = args.schedule
+    thr = args.threshold if args.threshold is not None else (3.0 if args.config == "C4" else 0.0)
 
     def step(pts, f, xe, alpha, s):
         h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=H.k)
-        h.assemble()
+        h.assemble(T=thr, lagrange_tol=1e-14)
         _, sinfo = h.solve(f, tol=args.tol, max_iter=20000, schedule=sched, alpha=alpha)
         _, einfo = h.evaluate(xe, out=s)
         hinfo = h.info()
@@ -220,7 +221,7 @@ def run_msk(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOAD if args.config == "C3" else args.config,
-                   "config": args.config, "schedule": sched, "tol": args.tol,
+                   "config": args.config, "schedule": sched, "tol": args.tol, "threshold_T": thr,
                    "n_per_level": H.n, "nnz_A": [int(hinfo.nnz_A[l]) for l in range(L)],
                    "cg_iters": [int(sinfo.cg_iters[l]) for l in range(L)],
                    "m_eval": int(H.eval_points.shape[0]),
@@ -324,6 +325,8 @@ def main():
     ap.add_argument("--m-eval", type=int, default=None)
     ap.add_argument("--schedule", default="pruned", choices=["pruned", "literal"])
     ap.add_argument("--tol", type=float, default=1e-12)
+    ap.add_argument("--threshold", type=float, default=None,
+                    help="T of the thresholded factor (C4 default 3; 0 = exact mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
