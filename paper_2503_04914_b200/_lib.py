@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsk.so")
+# MSK_LIB_PATH: development override (A/B timing of alternative in-tree builds)
+LIB_PATH = os.environ.get("MSK_LIB_PATH") or os.path.join(_HERE, "libmsk.so")
 
 MSK_OK, MSK_ERR_INVALID, MSK_ERR_NOMEM, MSK_ERR_CUDA, MSK_ERR_NCCL, MSK_ERR_NOCONV, MSK_ERR_STATE = range(7)
 MSK_SCHED_PRUNED = 0

@@ -1137,11 +1137,26 @@ extern "C" msk_status msk_cg_level(msk_hierarchy *h, int level, const double *b,
     int *d_it = dalloc<int>(2, st);
     double *d_rr = dalloc<double>(2, st);
     CGLevelArgs a = cg_args(h, level, tol, max_iter, nullptr, bd.ptr, xs, xd.ptr, d_it, d_rr, d_it + 1);
+    const bool phases = getenv("MSK_CG_PHASES") != nullptr;  // diagnostic phase timing
+    unsigned long long *dbg = nullptr;
+    if (phases) {
+        dbg = dalloc<unsigned long long>(6, st);
+        MSK_CUDA(cudaMemsetAsync(dbg, 0, 6 * sizeof(unsigned long long), st));
+        a.dbg = dbg;
+    }
     Timer tm(st);
     tm.start();
     cg_batched(&a, 1, st, nullptr);
     tm.stop();
     xd.flush();
+    if (phases) {
+        unsigned long long hd[6];
+        MSK_CUDA(cudaMemcpyAsync(hd, dbg, sizeof hd, cudaMemcpyDeviceToHost, st));
+        MSK_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[msk] cg phases (ms, CTA 0): spmv %.3f bar1 %.3f rupd %.3f bar2 %.3f pupd %.3f bar3 %.3f\n",
+                hd[0] * 1e-6, hd[1] * 1e-6, hd[2] * 1e-6, hd[3] * 1e-6, hd[4] * 1e-6, hd[5] * 1e-6);
+        dfree(dbg, st);
+    }
     int hit[2];
     double hrr[2];
     MSK_CUDA(cudaMemcpyAsync(hit, d_it, sizeof hit, cudaMemcpyDeviceToHost, st));

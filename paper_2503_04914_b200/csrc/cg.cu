@@ -43,9 +43,9 @@ namespace msk {
 namespace {
 constexpr int NT = 256;       // threads per CTA == rows per tile
 constexpr int NW = NT / 32;   // warps per CTA
-constexpr int CAPW = 320;     // CSR entries per warp pipeline stage (values 2.5 KB + columns 1.3 KB)
+constexpr int CAPW = 224;     // CSR entries per warp pipeline stage (values 1.75 KB + columns 0.9 KB)
 constexpr int CAPWE = CAPW - 2;  // usable entries per stage (16-byte alignment slack)
-constexpr int U = 8;          // independent gathers in flight per lane
+constexpr int U = 4;          // independent gathers in flight per lane (row-parallel)
 constexpr int MAXCH = 4;      // max tiles per chunk
 constexpr int RPCAP = MAXCH * NT + 4;  // staged row pointers per chunk
 
@@ -65,6 +65,22 @@ struct __align__(16) CGShared {
     double red[NT / 32 + 2];
     uint64_t bar;             // CTA barrier for the row-pointer copy
     uint64_t wbar[NW][2];     // per-warp, per-stage barriers
+};
+
+// ---- CTA-level pipeline (used by k_cg): large bulk copies, double-buffered
+constexpr int CAPT = 2048;        // CSR entries per stage (values 16 KB + columns 8 KB)
+constexpr int CAPTE = CAPT - 2;   // usable entries per piece (alignment slack)
+constexpr int NSTG = 2;           // pipeline stages (NSTG - 1 pieces in flight ahead)
+struct __align__(16) CtaStage {
+    double val[CAPT];
+    int32_t col[CAPT + 8];
+};
+struct __align__(16) CGSharedT {
+    CtaStage st[NSTG];        // ring of CSR slices (a stream of pieces)
+    int64_t rp[2][RPCAP];     // row pointers of the current and the next chunk
+    double red[NT / 32 + 2];
+    uint64_t bar_st[NSTG];
+    uint64_t bar_rp[2];
 };
 
 __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
@@ -171,24 +187,23 @@ __device__ __forceinline__ double spmv_warp(CGShared &S, int ro, int nrows, int6
         const int sj = (int)(j & 1u);
         mbar_wait(&bars[sj], (j >> 1) & 1u);
         WarpStage &cur = stg[sj];
-        const int voff = (int)(kb & 1), coff = (int)(kb & 3), m = (int)(ke - kb);
-        for (int e = lane; e < m; e += 32 * U) {
-            double pv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                int ee = e + u * 32;
-                pv[u] = ee < m ? p[cur.col[coff + ee]] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                int ee = e + u * 32;
-                if (ee < m) cur.val[voff + ee] *= pv[u];
-            }
-        }
-        __syncwarp();
+        const int voff = (int)(kb & 1), coff = (int)(kb & 3);
         {
-            int64_t lo = myb > kb ? myb : kb, hi = mye < ke ? mye : ke;
-            for (int64_t k = lo; k < hi; ++k) acc += cur.val[voff + (int)(k - kb)];
+            // row-parallel: each lane gathers its own row's columns of this
+            // piece (U independent loads in flight), ascending column order
+            const int lo = (int)((myb > kb ? myb : kb) - kb), hi = (int)((mye < ke ? mye : ke) - kb);
+            for (int e = lo; e < hi; e += U) {
+                double pv[U], vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int ee = e + u;
+                    pv[u] = ee < hi ? p[cur.col[coff + ee]] : 0.0;
+                    vv[u] = ee < hi ? cur.val[voff + ee] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (e + u < hi) acc = fma(vv[u], pv[u], acc);
+            }
         }
         if (ke == sub_end) {  // subtile s complete
             const int lr = s * 32 + lane;
@@ -246,9 +261,154 @@ __device__ __forceinline__ double spmv_chunk(CGShared &S, const int64_t *row_ptr
     return dot;
 }
 
+// ---------------------------------------------------------------------------
+// CTA-level pipelined SpMV phase: q = A p over all chunks of this CTA, with
+// pq partials per chunk.  The CTA's CSR entries are streamed as a sequence of
+// pieces (<= CAPTE entries, two bulk copies each) through two stages: piece
+// P+1 is in flight while piece P is consumed.  Row pointers of the next chunk
+// are prefetched into the second rp buffer.  Each thread owns row
+// t*NT + tid of every tile t of the chunk and gathers p for the entries of
+// its rows that fall into the piece (row-parallel, U loads in flight),
+// accumulating in ascending column order.
+struct PipeState {
+    uint32_t P;   // pieces consumed so far (stage P%NSTG, parity (P/NSTG)&1)
+    uint32_t CS;  // chunks visited so far (rp buffer CS&1, parity (CS>>1)&1)
+};
+
+__device__ __forceinline__ void issue_rp(CGSharedT &S, int b, const int64_t *row_ptr, int64_t r0, int nrows,
+                                         uint64_t pol) {
+    const int64_t lo = r0 & ~(int64_t)1;
+    const int64_t hi = (r0 + nrows + 2) & ~(int64_t)1;
+    const uint32_t bytes = (uint32_t)((hi - lo) * 8);
+    mbar_arrive_expect_tx(&S.bar_rp[b], bytes);
+    tma_load_1d(S.rp[b], row_ptr + lo, bytes, &S.bar_rp[b], pol);
+}
+
+__device__ __forceinline__ void issue_piece_t(CGSharedT &S, int b, const int32_t *col, const double *val,
+                                              int64_t kb, int64_t ke, uint64_t pol) {
+    const int64_t vlo = kb & ~(int64_t)1, vhi = (ke + 1) & ~(int64_t)1;
+    const int64_t clo = kb & ~(int64_t)3, chi = (ke + 3) & ~(int64_t)3;
+    const uint32_t vb = (uint32_t)((vhi - vlo) * 8), cb = (uint32_t)((chi - clo) * 4);
+    mbar_arrive_expect_tx(&S.bar_st[b], vb + cb);
+    tma_load_1d(S.st[b].val, val + vlo, vb, &S.bar_st[b], pol);
+    tma_load_1d(S.st[b].col, col + clo, cb, &S.bar_st[b], pol);
+}
+
+__device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, int me, int nb, int64_t nchunks,
+                                           int CH, double *part_out, PipeState &ps, uint64_t pol) {
+    const int tid = threadIdx.x;
+    const int64_t n = L.n;
+    const int64_t K = me < nchunks ? (nchunks - 1 - me) / nb + 1 : 0;  // my chunks
+    if (K == 0) return;
+    const double *p = L.p;  // written by other CTAs in earlier phases: coherent loads
+    auto chunk_rows = [&](int64_t k, int64_t &cr0, int &crows) {
+        const int64_t c = me + k * nb;
+        cr0 = c * CH * NT;
+        crows = (int)(n - cr0 < (int64_t)CH * NT ? n - cr0 : (int64_t)CH * NT);
+    };
+    auto rp_off = [&](int64_t cr0) { return (int)(cr0 - (cr0 & ~(int64_t)1)); };
+    int64_t cr0;
+    int crows;
+    if (tid == 0) {
+        chunk_rows(0, cr0, crows);
+        issue_rp(S, ps.CS & 1, L.row_ptr, cr0, crows, pol);
+        if (K > 1) {
+            chunk_rows(1, cr0, crows);
+            issue_rp(S, (ps.CS + 1) & 1, L.row_ptr, cr0, crows, pol);
+        }
+    }
+    mbar_wait(&S.bar_rp[ps.CS & 1], (ps.CS >> 1) & 1u);
+    chunk_rows(0, cr0, crows);
+    {
+        const int64_t *rp = S.rp[ps.CS & 1] + rp_off(cr0);
+        const int64_t K0 = rp[0], K1 = rp[crows];
+        if (tid == 0) issue_piece_t(S, ps.P & 1, L.col, L.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
+    }
+    for (int64_t k = 0; k < K; ++k) {
+        chunk_rows(k, cr0, crows);
+        const uint32_t cs = ps.CS + (uint32_t)k;
+        const int64_t *rp = S.rp[cs & 1] + rp_off(cr0);
+        const int64_t K1 = rp[crows];
+        int64_t rb[MAXCH], re[MAXCH];
+        double acc[MAXCH];
+#pragma unroll
+        for (int t = 0; t < MAXCH; ++t) {
+            const int r = t * NT + tid;
+            const bool ok = t < CH && r < crows;
+            rb[t] = ok ? rp[r] : 0;
+            re[t] = ok ? rp[r + 1] : 0;
+            acc[t] = 0.0;
+        }
+        for (int64_t kb = rp[0]; kb < K1;) {
+            const int64_t ke = kb + CAPTE < K1 ? kb + CAPTE : K1;
+            // the next piece (rest of this chunk, or the first piece of the next
+            // one) goes into the other stage, which held piece P-1 (consumed)
+            if (ke < K1) {
+                if (tid == 0)
+                    issue_piece_t(S, (ps.P + 1) & 1, L.col, L.val, ke, ke + CAPTE < K1 ? ke + CAPTE : K1, pol);
+            } else if (k + 1 < K) {
+                mbar_wait(&S.bar_rp[(cs + 1) & 1], ((cs + 1) >> 1) & 1u);
+                if (tid == 0) {
+                    int64_t nr0;
+                    int nrows;
+                    chunk_rows(k + 1, nr0, nrows);
+                    const int64_t *nrp = S.rp[(cs + 1) & 1] + rp_off(nr0);
+                    const int64_t a = nrp[0], e = nrp[nrows];
+                    issue_piece_t(S, (ps.P + 1) & 1, L.col, L.val, a, a + CAPTE < e ? a + CAPTE : e, pol);
+                }
+            }
+            mbar_wait(&S.bar_st[ps.P & 1], (ps.P >> 1) & 1u);
+            const CtaStage &cur = S.st[ps.P & 1];
+            const int voff = (int)(kb & 1), coff = (int)(kb & 3);
+#pragma unroll
+            for (int t = 0; t < MAXCH; ++t) {
+                if (t >= CH) break;
+                const int lo = (int)((rb[t] > kb ? rb[t] : kb) - kb);
+                const int hi = (int)((re[t] < ke ? re[t] : ke) - kb);
+                for (int e = lo; e < hi; e += U) {
+                    double pv[U], vv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int ee = e + u;
+                        pv[u] = ee < hi ? p[cur.col[coff + ee]] : 0.0;
+                        vv[u] = ee < hi ? cur.val[voff + ee] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (e + u < hi) acc[t] = fma(vv[u], pv[u], acc[t]);
+                }
+            }
+            __syncthreads();  // stage P%NSTG consumed by every thread: it may be refilled
+            ++ps.P;
+            kb = ke;
+        }
+        double dot = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXCH; ++t) {
+            const int r = t * NT + tid;
+            if (t < CH && r < crows) {
+                const int64_t i = cr0 + r;
+                L.q[i] = acc[t];
+                dot += p[i] * acc[t];
+            }
+        }
+        const double s = block_sum<NT>(dot, S.red);  // its barriers also retire rp buffer cs&1
+        if (tid == 0) {
+            part_out[me + k * nb] = s;
+            if (k + 2 < K) {
+                int64_t nr0;
+                int nrows;
+                chunk_rows(k + 2, nr0, nrows);
+                issue_rp(S, cs & 1, L.row_ptr, nr0, nrows, pol);
+            }
+        }
+    }
+    ps.CS += (uint32_t)K;
+}
+
 __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CGShared &S = *reinterpret_cast<CGShared *>(smem_raw);
+    CGSharedT &S = *reinterpret_cast<CGSharedT *>(smem_raw);
 
     int g = 0;
     while (g + 1 < B.nlev && (int)blockIdx.x >= B.lev[g + 1].block_begin) ++g;
@@ -261,9 +421,14 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
     const int64_t nchunks = (ntiles + CH - 1) / CH;
     double *part = L.partials;  // 3 * nchunks
     unsigned long long round = 0;
-    uint32_t phase = 0;
-    uint32_t J = 0;  // pieces consumed by this warp
-    init_barriers(S);
+    PipeState ps{0u, 0u};
+    if (tid == 0) {
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        mbar_init(&S.bar_rp[0], 1);
+        mbar_init(&S.bar_rp[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
     const uint64_t pol = policy_evict_first();
 
     // ---- init: x = 0, r = p = b, bb = b.b
@@ -285,24 +450,28 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
     const double bb = chunk_allreduce(part, nchunks, nb, L.barrier, round, S.red);
     double rr = bb;
     int it = 0, status = 0;
+    // optional phase timing (CTA 0 of the group, thread 0; MSK_CG_PHASES=1)
+    const bool tdbg = L.dbg != nullptr && me == 0 && tid == 0;
+    unsigned long long tph[6] = {0, 0, 0, 0, 0, 0}, tprev = 0;
+    auto tick = [&](int k) {
+        if (tdbg) {
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (k >= 0) tph[k] += now - tprev;
+            tprev = now;
+        }
+    };
     if (bb > 0.0) {
         const double stop = L.tol2 * bb;
         for (;;) {
             if (rr <= stop) break;
             if (it >= L.max_iter) { status = 1; break; }
+            tick(-1);
             // ---- q = A p, pq = p.q
-            {
-                const double *p = L.p;  // written by other CTAs in earlier phases: coherent loads
-                for (int64_t c = me; c < nchunks; c += nb) {
-                    const int64_t cr0 = c * CH * NT;
-                    const int crows = (int)(n - cr0 < (int64_t)CH * NT ? n - cr0 : (int64_t)CH * NT);
-                    double acc = spmv_chunk(S, L.row_ptr, L.col, L.val, p, L.q, cr0, crows, CH, phase,
-                                            J, pol);
-                    double s = block_sum<NT>(acc, S.red);
-                    if (tid == 0) part[nchunks + c] = s;
-                }
-            }
+            spmv_phase(S, L, me, nb, nchunks, CH, part + nchunks, ps, pol);
+            tick(0);
             const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, S.red);
+            tick(1);
             const double alpha = rr / pq;
             // ---- r -= alpha q, rr' = r.r
             {
@@ -331,7 +500,9 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
                     if (tid == 0) part[2 * nchunks + c] = s;
                 }
             }
+            tick(2);
             const double rrn = chunk_allreduce(part + 2 * nchunks, nchunks, nb, L.barrier, round, S.red);
+            tick(3);
             const double beta = rrn / rr;
             rr = rrn;
             // ---- x += alpha p, p = r + beta p
@@ -359,10 +530,14 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
                     }
                 }
             }
+            tick(4);
             group_barrier(L.barrier, nb, round);
+            tick(5);
             ++it;
         }
     }
+    if (tdbg)
+        for (int k = 0; k < 6; ++k) L.dbg[k] = tph[k];
     if (L.x_out) {
         for (int64_t c = me; c < nchunks; c += nb)
             for (int t = 0; t < CH; ++t) {
@@ -399,7 +574,7 @@ int g_max_resident = 0;
 void set_smem_attrs() {
     static bool done = false;
     if (done) return;
-    MSK_CUDA(cudaFuncSetAttribute(k_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
+    MSK_CUDA(cudaFuncSetAttribute(k_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGSharedT)));
     MSK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
     done = true;
 }
@@ -411,7 +586,7 @@ int cg_max_resident_blocks() {
         int dev = 0, sms = 0, per = 0;
         MSK_CUDA(cudaGetDevice(&dev));
         MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg, NT, sizeof(CGShared)));
+        MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg, NT, sizeof(CGSharedT)));
         g_max_resident = sms * (per > 0 ? per : 1);
     }
     return g_max_resident;
@@ -485,7 +660,7 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
         poff += 3 * nch[l];
     }
     void *args[] = {&B};
-    MSK_CUDA(cudaLaunchCooperativeKernel((void *)k_cg, dim3(used), dim3(NT), args, sizeof(CGShared), st));
+    MSK_CUDA(cudaLaunchCooperativeKernel((void *)k_cg, dim3(used), dim3(NT), args, sizeof(CGSharedT), st));
     if (launches) *launches += 1;
     MSK_CUDA(cudaFreeAsync(partials, st));
     MSK_CUDA(cudaFreeAsync(bars, st));

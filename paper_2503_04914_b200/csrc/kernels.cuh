@@ -85,6 +85,7 @@ struct CGLevelArgs {
     int *out_iters;           // device
     double *out_rr;           // device: final rr, bb
     int *out_status;          // device: 0 ok, 1 noconv
+    unsigned long long *dbg;  // optional: 6 phase times (ns) of CTA 0 (spmv, bar1, r, bar2, p, bar3)
 };
 // Run independent CGs on several levels in one cooperative launch.
 // CSR arrays must be 16-byte aligned and padded: row_ptr n+3 entries,
