@@ -778,10 +778,13 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 a = cg_args(h, l, tl, max_iter, h->ws_beta(l), nullptr, alpha_sp[l], ad[l].ptr,
                             d_it + l, d_rr + 2 * l, d_stat + l);
             }
+            debug_sync(st, "b_products");
             time_cg(l);
             cg_batched(&a, 1, st, &launches);
             cg_t.back()->stop();
+            debug_sync(st, "cg");
             if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);  // source records for later B products
+            debug_sync(st, "pack");
         }
     } else {
         // Literal Algorithm 2: beta_0 = f; L sweeps of

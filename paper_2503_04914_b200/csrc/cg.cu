@@ -191,7 +191,8 @@ __device__ __forceinline__ double spmv_warp(CGShared &S, int ro, int nrows, int6
         {
             // row-parallel: each lane gathers its own row's columns of this
             // piece (U independent loads in flight), ascending column order
-            const int lo = (int)((myb > kb ? myb : kb) - kb), hi = (int)((mye < ke ? mye : ke) - kb);
+            const int64_t lo64 = myb > kb ? myb : kb, hi64 = mye < ke ? mye : ke;  // 64-bit clamp
+            const int lo = (int)(lo64 - kb), hi = hi64 > lo64 ? (int)(hi64 - kb) : lo;
             for (int e = lo; e < hi; e += U) {
                 double pv[U], vv[U];
 #pragma unroll
@@ -363,8 +364,10 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
 #pragma unroll
             for (int t = 0; t < MAXCH; ++t) {
                 if (t >= CH) break;
-                const int lo = (int)((rb[t] > kb ? rb[t] : kb) - kb);
-                const int hi = (int)((re[t] < ke ? re[t] : ke) - kb);
+                // clamp in 64-bit before narrowing (entry offsets exceed 2^31)
+                const int64_t lo64 = rb[t] > kb ? rb[t] : kb, hi64 = re[t] < ke ? re[t] : ke;
+                const int lo = (int)(lo64 - kb);
+                const int hi = hi64 > lo64 ? (int)(hi64 - kb) : lo;
                 for (int e = lo; e < hi; e += U) {
                     double pv[U], vv[U];
 #pragma unroll

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <stdexcept>
 #include <string>
 
@@ -26,6 +28,16 @@ struct Error : std::runtime_error {
     } while (0)
 
 #define MSK_CHECK_LAUNCH() MSK_CUDA(cudaGetLastError())
+
+// MSK_DEBUG_SYNC=1: synchronise after each orchestrated launch and name the
+// failing step (diagnostics for device faults; off by default).
+inline void debug_sync(cudaStream_t st, const char *what) {
+    static int on = -1;
+    if (on < 0) on = getenv("MSK_DEBUG_SYNC") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) throw Error(3, std::string(what) + ": " + cudaGetErrorString(e));
+}
 
 constexpr int kMaxLevels = 16;
 

@@ -170,6 +170,12 @@ def config(name: str, m_eval=None) -> Hierarchy:
         return halton_hierarchy(name, 3, sizes, 1.5,
                                 m_eval=(10_000_000 if name == "C3" else 1_000_000 if name == "C4"
                                         else 100_000) if m_eval is None else m_eval)
+    if name.startswith("P") and name[1:].isdigit():
+        # paper workload (Table 1 / Figure 4): grids l=1..L, nu=4, phi_(3,1)
+        L = int(name[1:])
+        H = grid_hierarchy(L, m_eval=(100_000 if m_eval is None else m_eval))
+        H.name = name
+        return H
     if name == "C5":
         sizes = [int(round(5e7 * 4.0 ** (l - 8))) for l in range(1, 9)]
         return halton_hierarchy("C5", 2, sizes, 4.0,
