@@ -68,6 +68,9 @@ typedef enum {
 
 /* msk_hierarchy_create flags */
 #define MSK_FLAG_NONE 0u
+#define MSK_FLAG_DIST_ALL 1u /* distributed context: partition every level that has at least world
+                                row chunks (default: only levels with >= 2^20 points; smaller
+                                levels are solved redundantly on every rank) */
 
 /* msk_solve schedules */
 #define MSK_SCHED_PRUNED 0u  /* Algorithm 2 with each inner solve t^{(l)} = A_l^{-1} beta^{(l)} done
@@ -121,12 +124,40 @@ typedef struct {
 
 /* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t of
  * that device to enqueue on, or NULL to let the library create its own.
- * rank / world_size / nccl_unique_id: reserved for the partitioned
- * multi-GPU path; this version requires world_size == 1 (rank 0,
- * nccl_unique_id NULL) and returns MSK_ERR_INVALID otherwise. */
+ * Distribution (north_star: levels partitioned across the GPUs of one box by
+ * spatially sorted row blocks, halo exchange + reductions over NCCL):
+ *   world_size == 1: rank 0, nccl_unique_id NULL (single GPU);
+ *   world_size in 2..16, 0 <= rank < world_size, nccl_unique_id = the 128-byte
+ *     ncclUniqueId from msk_nccl_unique_id on rank 0 (broadcast by the caller,
+ *     e.g. with torch.distributed): one partition per rank over NCCL (the
+ *     libnccl already loaded by the process is used);
+ *   world_size in 2..16, rank == -1, nccl_unique_id NULL: single-process
+ *     emulation -- all world_size partitions run on this device and exchange
+ *     through device copies (used to test the partitioned path on one GPU).
+ * Every rank must pass identical inputs to every later call. */
 MSK_API msk_status msk_ctx_create(int device, void *cuda_stream, int rank, int world_size,
                           const void *nccl_unique_id, msk_ctx **out);
 MSK_API void msk_ctx_destroy(msk_ctx *ctx);
+
+/* out [host, 128 bytes]: a fresh ncclUniqueId (call on rank 0 only). */
+MSK_API msk_status msk_nccl_unique_id(void *out);
+
+/* Host-only row partition of a level of n points over `world` partitions:
+ * bounds [host, world+1] with partition r owning spatial rows
+ * [bounds[r], bounds[r+1]); boundaries fall on whole reduction chunks (DESIGN.md
+ * §Multi-GPU), so per-chunk partial sums are identical for every world size. */
+MSK_API msk_status msk_partition_rows(int64_t n, int world, int64_t *bounds);
+
+/* Host-only halo plan of partition `rank` for one partitioned level:
+ * rows [host, world+1] from msk_partition_rows; hlo/hhi [host, world]: the
+ * column range [hlo[s], hhi[s]) referenced by partition s's rows (its own rows
+ * included).  Outputs [host, world each]: partition `rank` sends its rows
+ * [send_lo[s], send_hi[s]) of p to s and receives rows [recv_lo[s],
+ * recv_hi[s]) from s before every SpMV (empty ranges have lo == hi; s == rank
+ * is always empty). */
+MSK_API msk_status msk_halo_plan(int world, int rank, const int64_t *rows, const int64_t *hlo,
+                                 const int64_t *hhi, int64_t *send_lo, int64_t *send_hi, int64_t *recv_lo,
+                                 int64_t *recv_hi);
 
 /* ------------------------------------------------------------- hierarchy */
 

@@ -16,7 +16,7 @@ import weakref
 import numpy as np
 
 from . import _lib
-from ._lib import (EXPORTED, MSK_SCHED_LITERAL, MSK_SCHED_PRUNED, EvalInfo, HierarchyInfo,
+from ._lib import (EXPORTED, MSK_FLAG_DIST_ALL, MSK_SCHED_LITERAL, MSK_SCHED_PRUNED, EvalInfo, HierarchyInfo,
                    MskError, SolveInfo, check, load)
 
 __all__ = ["Context", "Hierarchy", "MskError", "SolveInfo", "HierarchyInfo", "EvalInfo",
@@ -152,6 +152,25 @@ def msk_cg_level(h, level, b, x, tol, max_iter):
     return it.value, rr.value, t.value
 
 
+def msk_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(load().msk_nccl_unique_id(ctypes.cast(buf, _vp)))
+    return buf.raw
+
+
+def msk_partition_rows(n, world):
+    b = (ctypes.c_int64 * (world + 1))()
+    check(load().msk_partition_rows(int(n), int(world), b))
+    return list(b)
+
+
+def msk_halo_plan(world, rank, rows, hlo, hhi):
+    arr = lambda v: (ctypes.c_int64 * len(v))(*[int(x) for x in v])
+    out = [(ctypes.c_int64 * world)() for _ in range(4)]
+    check(load().msk_halo_plan(int(world), int(rank), arr(rows), arr(hlo), arr(hhi), *out))
+    return [list(o) for o in out]  # send_lo, send_hi, recv_lo, recv_hi
+
+
 def msk_last_error():
     return load().msk_last_error().decode()
 
@@ -162,11 +181,36 @@ def msk_version():
 
 # ----------------------------------------------------------------- handles
 class Context:
-    """A libmsk context on one CUDA device (world_size 1)."""
+    """A libmsk context on one CUDA device.
 
-    def __init__(self, device: int = 0, stream=None):
-        self.handle = msk_ctx_create(device, stream)
+    world == 1: single GPU.  world > 1 with rank >= 0: one partition per rank
+    over NCCL; `nccl_id` is the 128-byte id from msk_nccl_unique_id() on rank
+    0 (``Context.distributed`` broadcasts it with torch.distributed).
+    world > 1 with rank == -1: single-process emulation of `world` partitions
+    on this device (tests).
+    """
+
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id=None):
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self.rank, self.world = rank, world
+        self.handle = msk_ctx_create(device, stream, rank, world,
+                                     ctypes.cast(idbuf, _vp) if idbuf is not None else None)
         self._children = weakref.WeakSet()
+
+    @classmethod
+    def distributed(cls, device: int, stream=None):
+        """One rank of a torch.distributed job: rank 0 creates the NCCL id and
+        broadcasts it through the process group (plumbing only)."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if world == 1:
+            return cls(device, stream)
+        obj = [msk_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(device, stream, rank, world, obj[0])
 
     def close(self):
         if self.handle:
@@ -189,14 +233,14 @@ class Hierarchy:
     delta:  support radii; q: separation values or None; k: Wendland phi_{d,k}.
     """
 
-    def __init__(self, ctx: Context, points, delta, q=None, k: int = 1):
+    def __init__(self, ctx: Context, points, delta, q=None, k: int = 1, flags: int = 0):
         pts = [_f64(p) for p in points]
         self.ctx = ctx
         self.d = int(pts[0].shape[1])
         self.L = len(pts)
         self.n = [int(p.shape[0]) for p in pts]
         self.handle = msk_hierarchy_create(ctx.handle, self.d, self.L, self.n, pts, list(delta),
-                                           None if q is None else list(q), int(k))
+                                           None if q is None else list(q), int(k), int(flags))
         self.last_solve = None
         ctx._children.add(self)
 

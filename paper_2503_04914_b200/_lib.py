@@ -86,6 +86,9 @@ def load() -> ctypes.CDLL:
         "msk_apply_block": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.POINTER(_dbl)], ctypes.c_int),
         "msk_cg_level": ([_vp, ctypes.c_int, _vp, _vp, _dbl, _i32, ctypes.POINTER(_i32),
                           ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)], ctypes.c_int),
+        "msk_nccl_unique_id": ([_vp], ctypes.c_int),
+        "msk_partition_rows": ([_i64, ctypes.c_int, ctypes.POINTER(_i64)], ctypes.c_int),
+        "msk_halo_plan": ([ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(_i64)] * 7, ctypes.c_int),
         "msk_last_error": ([], ctypes.c_char_p),
         "msk_version": ([], ctypes.c_char_p),
     }
@@ -100,7 +103,8 @@ def load() -> ctypes.CDLL:
 EXPORTED = ["msk_ctx_create", "msk_ctx_destroy", "msk_hierarchy_create", "msk_hierarchy_destroy",
             "msk_hierarchy_info_get", "msk_assemble", "msk_solve", "msk_evaluate", "msk_evaluate_ex",
             "msk_export_block", "msk_export_factor", "msk_export_cells", "msk_apply_block", "msk_cg_level",
-            "msk_last_error", "msk_version"]
+            "msk_nccl_unique_id", "msk_partition_rows", "msk_halo_plan", "msk_last_error", "msk_version"]
+MSK_FLAG_DIST_ALL = 1
 
 
 def check(status: int) -> None:

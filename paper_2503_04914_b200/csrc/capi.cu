@@ -20,6 +20,7 @@
 
 #include "../../include/msk.h"
 #include "kernels.cuh"
+#include "nccl_dl.cuh"
 
 using namespace msk;
 
@@ -28,6 +29,12 @@ struct msk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // distributed solve: world partitions of every
+    // large level; `emulated` runs all partitions in this process on one
+    // device (testing), else one partition per rank over NCCL.
+    int rank = 0, world = 1;
+    bool emulated = false;
+    ncclComm_t comm = nullptr;
 };
 
 namespace {
@@ -189,6 +196,32 @@ struct msk_hierarchy {
     double *tval = nullptr;
     int lagrange_max_iters = 0;
     double t_lagrange_ms = 0;
+    // distributed solve: per level, the row partition and this process's
+    // partitions (one per rank over NCCL, all of them in the emulation)
+    uint32_t flags = 0;
+    struct PartLocal {
+        int rank = 0;
+        int64_t lo = 0, hi = 0, c0 = 0, c1 = 0, nnz = 0;
+        int64_t *rp = nullptr;   // owned rows' CSR (local entries, global columns)
+        int32_t *col = nullptr;
+        double *val = nullptr;
+        int64_t hlo = 0, hhi = 0;  // columns referenced by the owned rows: [hlo, hhi)
+    };
+    struct LevelDist {
+        bool on = false;
+        std::vector<int64_t> rows;       // world + 1 row bounds
+        std::vector<int64_t> hlo, hhi;   // per rank
+        std::vector<PartLocal> local;
+    };
+    LevelDist dist[kMaxLevels];
+
+    void release_dist() {
+        cudaStream_t s = st();
+        for (int l = 0; l < kMaxLevels; ++l) {
+            for (auto &P : dist[l].local) { dfree(P.rp, s); dfree(P.col, s); dfree(P.val, s); }
+            dist[l] = LevelDist();
+        }
+    }
 
     void release_factor() {
         cudaStream_t s = st();
@@ -244,6 +277,7 @@ struct msk_hierarchy {
         dfree(ws, s);
         ws = nullptr;
         release_factor();
+        release_dist();
     }
 };
 
@@ -253,19 +287,32 @@ extern "C" msk_status msk_ctx_create(int device, void *cuda_stream, int rank, in
     API_BEGIN
     require(out != nullptr, "msk_ctx_create: out is NULL");
     *out = nullptr;
-    require(world_size == 1 && rank == 0 && nccl_unique_id == nullptr,
-            "msk_ctx_create: only world_size == 1 is supported by this version");
+    require(world_size >= 1 && world_size <= kMaxParts, "msk_ctx_create: world_size must be in 1..16");
+    const bool emulated = world_size > 1 && rank == -1 && nccl_unique_id == nullptr;
+    if (world_size == 1) require(rank == 0 && nccl_unique_id == nullptr, "msk_ctx_create: world_size 1 needs rank 0, no id");
+    else if (!emulated)
+        require(rank >= 0 && rank < world_size && nccl_unique_id != nullptr,
+                "msk_ctx_create: distributed context needs 0 <= rank < world_size and an NCCL unique id "
+                "(or rank = -1 and no id for the single-process emulation)");
     int ndev = 0;
     MSK_CUDA(cudaGetDeviceCount(&ndev));
     require(device >= 0 && device < ndev, "msk_ctx_create: bad device index");
     MSK_CUDA(cudaSetDevice(device));
     msk_ctx *c = new msk_ctx();
     c->device = device;
+    c->world = world_size;
+    c->rank = emulated ? 0 : rank;
+    c->emulated = emulated;
     if (cuda_stream) {
         c->stream = (cudaStream_t)cuda_stream;
     } else {
         MSK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
+    }
+    if (world_size > 1 && !emulated) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof id);
+        MSK_NCCL(nccl_api()->CommInitRank(&c->comm, world_size, id, rank));
     }
     // keep freed blocks in the stream-ordered pool: repeated create/solve
     // cycles then allocate without device-wide synchronisation
@@ -282,8 +329,59 @@ extern "C" void msk_ctx_destroy(msk_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
+}
+
+extern "C" msk_status msk_nccl_unique_id(void *out) {
+    API_BEGIN
+    require(out != nullptr, "msk_nccl_unique_id: NULL argument");
+    ncclUniqueId id;
+    MSK_NCCL(nccl_api()->GetUniqueId(&id));
+    memcpy(out, &id, sizeof id);
+    API_END
+}
+
+// Halo plan of partition `rank` (host logic, no device): for every peer s,
+// the rows it must send to s (the part of s's referenced column range
+// [hlo[s], hhi[s]) that `rank` owns) and the rows it receives from s (the
+// part of its own referenced range that s owns).  Empty ranges have lo == hi.
+extern "C" msk_status msk_halo_plan(int world, int rank, const int64_t *rows, const int64_t *hlo,
+                                    const int64_t *hhi, int64_t *send_lo, int64_t *send_hi, int64_t *recv_lo,
+                                    int64_t *recv_hi) {
+    API_BEGIN
+    require(world >= 1 && rank >= 0 && rank < world && rows && hlo && hhi && send_lo && send_hi && recv_lo &&
+                recv_hi,
+            "msk_halo_plan: bad argument");
+    for (int s = 0; s < world; ++s) {
+        int64_t a = 0, b = 0, c = 0, e = 0;
+        if (s != rank) {
+            a = std::max(hlo[s], rows[rank]);
+            b = std::min(hhi[s], rows[rank + 1]);
+            c = std::max(hlo[rank], rows[s]);
+            e = std::min(hhi[rank], rows[s + 1]);
+        }
+        send_lo[s] = a;
+        send_hi[s] = std::max(a, b);
+        recv_lo[s] = c;
+        recv_hi[s] = std::max(c, e);
+    }
+    API_END
+}
+
+// Row partition of a level (host logic, no device): whole chunks of
+// cg_chunk_tiles(n) * 256 rows, chunks split as evenly as possible.
+extern "C" msk_status msk_partition_rows(int64_t n, int world, int64_t *bounds) {
+    API_BEGIN
+    require(n >= 0 && world >= 1 && bounds != nullptr, "msk_partition_rows: bad argument");
+    const int64_t rows_per_chunk = (int64_t)cg_chunk_tiles(n) * 256;
+    const int64_t nch = (n + rows_per_chunk - 1) / rows_per_chunk;
+    for (int r = 0; r <= world; ++r) {
+        const int64_t c = nch * r / world;
+        bounds[r] = std::min(c * rows_per_chunk, n);
+    }
+    API_END
 }
 
 // =============================================================== hierarchy
@@ -298,7 +396,7 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
         require(d == 2 || d == 3, "msk_hierarchy_create: d must be 2 or 3");
         require(L >= 1 && L <= kMaxLevels, "msk_hierarchy_create: L must be in 1..16");
         require(wendland_k >= 0 && wendland_k <= 2, "msk_hierarchy_create: k must be 0, 1 or 2");
-        require(flags == MSK_FLAG_NONE, "msk_hierarchy_create: unknown flags");
+        require((flags & ~MSK_FLAG_DIST_ALL) == 0, "msk_hierarchy_create: unknown flags");
         for (int l = 0; l < L; ++l) {
             require(n[l] >= 1 && n[l] < (1ll << 31) - 1, "msk_hierarchy_create: n[l] out of range");
             require(points[l] != nullptr, "msk_hierarchy_create: NULL points");
@@ -312,6 +410,7 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
         h->d = d;
         h->L = L;
         h->k = wendland_k;
+        h->flags = flags;
         Timer tm(st);
         tm.start();
         int launches = 0;
@@ -568,16 +667,53 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
     require(std::isfinite(T), "msk_assemble: T must be finite");
     require(!(T > 0.0) || (lagrange_tol > 0.0 && lagrange_tol < 1.0),
             "msk_assemble: lagrange_tol must be in (0,1) when T > 0");
+    require(!(T > 0.0) || h->ctx->world == 1, "msk_assemble: the thresholded factor is single-GPU in this version");
     MSK_CUDA(cudaSetDevice(h->ctx->device));
     cudaStream_t st = h->st();
     h->release_factor();
+    h->release_dist();
     Timer tm(st);
     tm.start();
     int launches = 0;
     std::vector<int64_t> nnz(h->L);
+    // distributed context: partition the large levels
+    const int W = h->ctx->world;
+    for (int l = 0; l < h->L && W > 1; ++l) {
+        const int64_t n = h->lev[l].n;
+        const int64_t rpc = (int64_t)cg_chunk_tiles(n) * 256;
+        const int64_t nch = (n + rpc - 1) / rpc;
+        if (nch >= W && ((h->flags & MSK_FLAG_DIST_ALL) || n >= (1ll << 20))) {
+            auto &Dd = h->dist[l];
+            Dd.on = true;
+            Dd.rows.resize(W + 1);
+            msk_partition_rows(n, W, Dd.rows.data());
+            for (int r = 0; r < W; ++r) {
+                if (!h->ctx->emulated && r != h->ctx->rank) continue;
+                msk_hierarchy::PartLocal P;
+                P.rank = r;
+                P.lo = Dd.rows[r];
+                P.hi = Dd.rows[r + 1];
+                P.c0 = P.lo / rpc;
+                P.c1 = (P.hi + rpc - 1) / rpc;
+                Dd.local.push_back(P);
+            }
+        }
+    }
     for (int l = 0; l < h->L; ++l) {
         LevelData &D = h->lev[l];
         dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st);
+        D.row_ptr = nullptr; D.col = nullptr; D.val = nullptr;
+        nnz[l] = 0;
+        if (h->dist[l].on) {  // owned rows only, per local partition
+            for (auto &P : h->dist[l].local) {
+                const int64_t m = P.hi - P.lo;
+                P.rp = dalloc<int64_t>((size_t)(m + 3), st);
+                MSK_CUDA(cudaMemsetAsync(P.rp + m + 1, 0, 2 * sizeof(int64_t), st));
+                exclusive_scan_i64(D.cnt + P.lo, m, P.rp, st, &launches);
+                MSK_CUDA(cudaMemcpyAsync(&P.nnz, P.rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            }
+            continue;
+        }
         D.row_ptr = dalloc<int64_t>((size_t)(D.n + 3), st);  // + padding for 16-byte bulk copies
         MSK_CUDA(cudaMemsetAsync(D.row_ptr + D.n + 1, 0, 2 * sizeof(int64_t), st));
         exclusive_scan_i64(D.cnt, D.n, D.row_ptr, st, &launches);
@@ -586,6 +722,45 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
     MSK_CUDA(cudaStreamSynchronize(st));
     for (int l = 0; l < h->L; ++l) {
         LevelData &D = h->lev[l];
+        if (h->dist[l].on) {
+            auto &Dd = h->dist[l];
+            unsigned long long *mm = dalloc<unsigned long long>(2, st);
+            for (auto &P : Dd.local) {
+                P.col = dalloc<int32_t>((size_t)P.nnz + 4, st);
+                P.val = dalloc<double>((size_t)P.nnz + 2, st);
+                MSK_CUDA(cudaMemsetAsync(P.col + P.nnz, 0, 4 * sizeof(int32_t), st));
+                MSK_CUDA(cudaMemsetAsync(P.val + P.nnz, 0, 2 * sizeof(double), st));
+                LevelView rows = h->view(l), cols = h->view(l);
+                rows.n = P.hi - P.lo;
+                for (int a = 0; a < h->d; ++a) rows.x[a] += P.lo;
+                fill_pattern(h->d, h->k, rows, cols, P.rp, P.col, P.val, st, &launches);
+                col_minmax(P.nnz, P.col, mm, st);
+                unsigned long long hm[2];
+                MSK_CUDA(cudaMemcpyAsync(hm, mm, sizeof hm, cudaMemcpyDeviceToHost, st));
+                MSK_CUDA(cudaStreamSynchronize(st));
+                P.hlo = P.nnz ? std::min<int64_t>((int64_t)hm[0], P.lo) : P.lo;
+                P.hhi = P.nnz ? std::max<int64_t>((int64_t)hm[1] + 1, P.hi) : P.hi;
+                D.nnz += P.nnz;
+            }
+            dfree(mm, st);
+            // every partition's halo range, known to all
+            Dd.hlo.assign(W, 0);
+            Dd.hhi.assign(W, 0);
+            if (h->ctx->emulated) {
+                for (auto &P : Dd.local) { Dd.hlo[P.rank] = P.hlo; Dd.hhi[P.rank] = P.hhi; }
+            } else {
+                int64_t *buf = dalloc<int64_t>((size_t)(2 * W + 2), st);
+                int64_t mine[2] = {Dd.local[0].hlo, Dd.local[0].hhi};
+                MSK_CUDA(cudaMemcpyAsync(buf + 2 * W, mine, sizeof mine, cudaMemcpyHostToDevice, st));
+                MSK_NCCL(nccl_api()->AllGather(buf + 2 * W, buf, 2, ncclInt64, h->ctx->comm, st));
+                std::vector<int64_t> all((size_t)(2 * W));
+                MSK_CUDA(cudaMemcpyAsync(all.data(), buf, sizeof(int64_t) * 2 * W, cudaMemcpyDeviceToHost, st));
+                MSK_CUDA(cudaStreamSynchronize(st));
+                for (int r = 0; r < W; ++r) { Dd.hlo[r] = all[2 * r]; Dd.hhi[r] = all[2 * r + 1]; }
+                dfree(buf, st);
+            }
+            continue;
+        }
         D.nnz = nnz[l];
         D.col = dalloc<int32_t>((size_t)D.nnz + 4, st);  // + padding for 16-byte bulk copies
         D.val = dalloc<double>((size_t)D.nnz + 2, st);
@@ -725,6 +900,165 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         alpha_sp[l] = h->lev[l].alpha;
         t_sp[l] = h->ws_t(l);
     }
+
+    // ---- distributed solve of one partitioned level:
+    // beta on the owned rows, then the CG as phase kernels with all-reduced
+    // chunk partials and halo exchange of p; alpha assembled on every rank.
+    auto dist_level = [&](int l, double tl) {
+        auto &Dd = h->dist[l];
+        LevelData &D = h->lev[l];
+        const int64_t n = D.n;
+        const int CH = cg_chunk_tiles(n);
+        const int64_t nch = (n + (int64_t)CH * 256 - 1) / ((int64_t)CH * 256);
+        const int np = (int)Dd.local.size();
+        const bool emu = h->ctx->emulated;
+        std::vector<double *> X(np), R(np), Pv(np), Q(np), send(np);
+        std::vector<double *> owned_alloc;
+        double *recv = dalloc<double>((size_t)nch, st);
+        DistCGScalars *sc = dalloc<DistCGScalars>((size_t)np, st);
+        for (int i = 0; i < np; ++i) {
+            if (emu) {
+                double *blk = dalloc<double>((size_t)(4 * n), st);
+                owned_alloc.push_back(blk);
+                X[i] = blk; R[i] = blk + n; Pv[i] = blk + 2 * n; Q[i] = blk + 3 * n;
+            } else {
+                X[i] = h->ws_t(l); R[i] = h->ws_r(l); Pv[i] = h->ws_p(l); Q[i] = h->ws_q(l);
+            }
+            send[i] = dalloc<double>((size_t)nch, st);
+            MSK_CUDA(cudaMemsetAsync(send[i], 0, sizeof(double) * (size_t)nch, st));
+        }
+        // beta^(l) on the owned rows (B products of the coarser, complete levels)
+        if (l > 0) {
+            for (auto &P : Dd.local) {
+                GatherArgs ga{};
+                ga.d = h->d;
+                ga.k = h->k;
+                ga.nt = P.hi - P.lo;
+                for (int a = 0; a < h->d; ++a) ga.tx[a] = D.xs + (size_t)a * n + P.lo;
+                ga.nlev = l;
+                for (int k = 0; k < l; ++k) ga.lev[k] = h->view(k, alpha_sp[k]);
+                ga.base = fd[l].ptr;
+                ga.base_perm = D.perm + P.lo;
+                ga.sign = -1.0;
+                ga.out = h->ws_beta(l) + P.lo;
+                ga.hits = d_hits;
+                time_ga();
+                gather(ga, st, &launches);
+                ga_t.back()->stop();
+            }
+        }
+        std::vector<DistCGArgs> args(np);
+        for (int i = 0; i < np; ++i) {
+            const auto &P = Dd.local[i];
+            DistCGArgs &A = args[i];
+            A.L = cg_args(h, l, tl, max_iter, l == 0 ? nullptr : h->ws_beta(l), l == 0 ? fd[0].ptr : nullptr,
+                          X[i], nullptr, nullptr, nullptr, nullptr);
+            A.L.r = R[i];
+            A.L.p = Pv[i];
+            A.L.q = Q[i];
+            A.L.row_ptr = P.rp - P.lo;  // indexed by global row
+            A.L.col = P.col;
+            A.L.val = P.val;
+            A.L.nnz = P.nnz;
+            A.L.chunk_tiles = CH;
+            A.c0 = P.c0;
+            A.c1 = P.c1;
+            A.nchunks = nch;
+            A.part_send = send[i];
+            A.part_recv = recv;
+            A.sc = sc + i;
+        }
+        auto allreduce = [&]() {
+            if (emu) {
+                DistPtrs ptrs{};
+                for (int i = 0; i < np; ++i) ptrs.p[i] = send[i];
+                sum_arrays(np, ptrs, recv, nch, st);
+            } else {
+                MSK_NCCL(nccl_api()->AllReduce(send[0], recv, (size_t)nch, ncclFloat64, ncclSum, h->ctx->comm, st));
+            }
+        };
+        // halo plans (msk_halo_plan): per local partition, send/recv row ranges per peer
+        const int W = h->ctx->world;
+        std::vector<std::vector<int64_t>> sl(np, std::vector<int64_t>(W)), sh = sl, rl = sl, rh = sl;
+        for (int i = 0; i < np; ++i)
+            msk_halo_plan(W, Dd.local[i].rank, Dd.rows.data(), Dd.hlo.data(), Dd.hhi.data(), sl[i].data(),
+                          sh[i].data(), rl[i].data(), rh[i].data());
+        auto halo = [&]() {
+            if (emu) {  // partition i receives from partition s by a device copy
+                for (int i = 0; i < np; ++i)
+                    for (int s = 0; s < W; ++s)
+                        if (rl[i][s] < rh[i][s])
+                            MSK_CUDA(cudaMemcpyAsync(Pv[i] + rl[i][s], Pv[s] + rl[i][s],
+                                                     sizeof(double) * (size_t)(rh[i][s] - rl[i][s]),
+                                                     cudaMemcpyDeviceToDevice, st));
+            } else {
+                MSK_NCCL(nccl_api()->GroupStart());
+                for (int s = 0; s < W; ++s) {
+                    if (sl[0][s] < sh[0][s])
+                        MSK_NCCL(nccl_api()->Send(Pv[0] + sl[0][s], (size_t)(sh[0][s] - sl[0][s]), ncclFloat64, s,
+                                                  h->ctx->comm, st));
+                    if (rl[0][s] < rh[0][s])
+                        MSK_NCCL(nccl_api()->Recv(Pv[0] + rl[0][s], (size_t)(rh[0][s] - rl[0][s]), ncclFloat64, s,
+                                                  h->ctx->comm, st));
+                }
+                MSK_NCCL(nccl_api()->GroupEnd());
+            }
+        };
+        time_cg(l);
+        for (int i = 0; i < np; ++i) dcg_init(args[i], st);
+        allreduce();
+        for (int i = 0; i < np; ++i) dcg_scalar(args[i], 0, st);
+        halo();
+        launches += 3 * np;
+        for (int done = 0;;) {
+            for (int k = 0; k < 8; ++k) {
+                for (int i = 0; i < np; ++i) dcg_spmv(args[i], st);
+                allreduce();
+                for (int i = 0; i < np; ++i) dcg_scalar(args[i], 1, st);
+                for (int i = 0; i < np; ++i) dcg_rupd(args[i], st);
+                allreduce();
+                for (int i = 0; i < np; ++i) dcg_scalar(args[i], 2, st);
+                for (int i = 0; i < np; ++i) dcg_xpupd(args[i], st);
+                for (int i = 0; i < np; ++i) dcg_scalar(args[i], 3, st);
+                halo();
+                launches += 7 * np + (emu ? 2 : 0);
+            }
+            done += 8;
+            DistCGScalars hs;
+            MSK_CUDA(cudaMemcpyAsync(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+            MSK_CUDA(cudaStreamSynchronize(st));
+            if (!hs.active || done > max_iter + 16) break;
+        }
+        cg_t.back()->stop();
+        // alpha^(l) complete on every rank (spatial order), then caller order
+        if (emu) {
+            for (int i = 0; i < np; ++i) {
+                const auto &P = Dd.local[i];
+                MSK_CUDA(cudaMemcpyAsync(alpha_sp[l] + P.lo, X[i] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
+                                         cudaMemcpyDeviceToDevice, st));
+            }
+        } else {
+            const auto &P = Dd.local[0];
+            double *tmp = Q[0];
+            MSK_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * (size_t)n, st));
+            MSK_CUDA(cudaMemcpyAsync(tmp + P.lo, X[0] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
+                                     cudaMemcpyDeviceToDevice, st));
+            MSK_NCCL(nccl_api()->AllReduce(tmp, alpha_sp[l], (size_t)n, ncclFloat64, ncclSum, h->ctx->comm, st));
+        }
+        permute_scatter(n, alpha_sp[l], D.perm, ad[l].ptr, st, &launches);
+        MSK_CUDA(cudaMemcpyAsync(d_it + l, &sc->it, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        MSK_CUDA(cudaMemcpyAsync(d_stat + l, &sc->status, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        MSK_CUDA(cudaMemcpyAsync(d_rr + 2 * l, &sc->rr, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        MSK_CUDA(cudaMemcpyAsync(d_rr + 2 * l + 1, &sc->bb, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        for (double *p : owned_alloc) dfree(p, st);
+        for (double *p : send) dfree(p, st);
+        dfree(recv, st);
+        dfree(sc, st);
+    };
+    bool any_dist = false;
+    for (int l = 0; l < L; ++l) any_dist = any_dist || h->dist[l].on;
+    require(!any_dist || schedule == MSK_SCHED_PRUNED, "msk_solve: a distributed solve uses the PRUNED schedule");
+
     const bool thresholded = h->T > 0.0;
     if (thresholded) {
         // a7: Jacobi on (id - M~(T)) beta = f (eq:perturbed_split P:865-869),
@@ -769,6 +1103,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         // same solve); the finest level is solved at tol.
         for (int l = 0; l < L; ++l) {
             const double tl = l + 1 < L ? inner_tol : tol;
+            if (h->dist[l].on) {
+                dist_level(l, tl);
+                debug_sync(st, "dist_level");
+                if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);
+                continue;
+            }
             CGLevelArgs a;
             if (l == 0) {
                 a = cg_args(h, l, tl, max_iter, nullptr, fd[0].ptr, alpha_sp[l], ad[l].ptr,
@@ -902,26 +1242,36 @@ extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double 
     co.perm = perm;
     for (int a = 0; a < d; ++a) co.xs[a] = xs + (size_t)a * m;
     co.cell_start = cs;
+    // distributed context: a stable sort makes the order identical on every
+    // rank, and each partition evaluates one contiguous share of it
+    const int W = h->ctx->world;
     tsort.start();
-    build_cell_list(d, m, xd.ptr, g, false, co, st, &launches);
+    build_cell_list(d, m, xd.ptr, g, W > 1, co, st, &launches);
     tsort.stop();
     unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
     MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
-    GatherArgs ga{};
-    ga.d = d;
-    ga.k = h->k;
-    ga.nt = m;
-    for (int a = 0; a < d; ++a) ga.tx[a] = xs + (size_t)a * m;
-    ga.nlev = L;
     for (int l = 0; l < L; ++l) h->pack(l, h->lev[l].alpha, &launches);
-    for (int l = 0; l < L; ++l) ga.lev[l] = h->view(l, h->lev[l].alpha);
-    ga.base = nullptr;
-    ga.sign = 1.0;
-    ga.out = sd.ptr;
-    ga.out_perm = perm;
-    ga.hits = d_hits;
+    if (W > 1) MSK_CUDA(cudaMemsetAsync(sd.ptr, 0, sizeof(double) * (size_t)m, st));
     teval.start();
-    gather(ga, st, &launches);
+    for (int r = 0; r < W; ++r) {
+        if (W > 1 && !h->ctx->emulated && r != h->ctx->rank) continue;
+        const int64_t lo = m * r / W, hi = m * (r + 1) / W;
+        GatherArgs ga{};
+        ga.d = d;
+        ga.k = h->k;
+        ga.nt = hi - lo;
+        for (int a = 0; a < d; ++a) ga.tx[a] = xs + (size_t)a * m + lo;
+        ga.nlev = L;
+        for (int l = 0; l < L; ++l) ga.lev[l] = h->view(l, h->lev[l].alpha);
+        ga.base = nullptr;
+        ga.sign = 1.0;
+        ga.out = sd.ptr;
+        ga.out_perm = perm + lo;
+        ga.hits = d_hits;
+        gather(ga, st, &launches);
+    }
+    if (W > 1 && !h->ctx->emulated)
+        MSK_NCCL(nccl_api()->AllReduce(sd.ptr, sd.ptr, (size_t)m, ncclFloat64, ncclSum, h->ctx->comm, st));
     teval.stop();
     sd.flush();
     ttot.stop();
@@ -960,7 +1310,7 @@ extern "C" msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_
     double *vl = nullptr;
     bool own = true;
     int64_t nnz = 0;
-    if (row_level == col_level && h->assembled) {
+    if (row_level == col_level && h->assembled && !h->dist[row_level].on) {
         rp = R.row_ptr; cl = R.col; vl = R.val; nnz = R.nnz;
         own = false;
     } else {
@@ -1085,6 +1435,8 @@ extern "C" msk_status msk_apply_block(msk_hierarchy *h, int row_level, int col_l
     require(row_level >= 0 && row_level < h->L && col_level >= 0 && col_level <= row_level,
             "msk_apply_block: need 0 <= col_level <= row_level < L");
     if (row_level == col_level && !h->assembled) throw Error(MSK_ERR_STATE, "msk_apply_block: assemble first");
+    if (row_level == col_level && h->dist[row_level].on)
+        throw Error(MSK_ERR_STATE, "msk_apply_block: level is partitioned across ranks");
     MSK_CUDA(cudaSetDevice(h->ctx->device));
     cudaStream_t st = h->st();
     const LevelData &R = h->lev[row_level], &C = h->lev[col_level];
@@ -1130,6 +1482,7 @@ extern "C" msk_status msk_cg_level(msk_hierarchy *h, int level, const double *b,
     require(level >= 0 && level < h->L, "msk_cg_level: bad level");
     require(tol > 0.0 && tol < 1.0 && max_iter >= 1, "msk_cg_level: bad tol / max_iter");
     if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_cg_level: assemble first");
+    if (h->dist[level].on) throw Error(MSK_ERR_STATE, "msk_cg_level: level is partitioned across ranks");
     MSK_CUDA(cudaSetDevice(h->ctx->device));
     cudaStream_t st = h->st();
     h->ensure_ws();

@@ -295,15 +295,18 @@ __device__ __forceinline__ void issue_piece_t(CGSharedT &S, int b, const int32_t
     tma_load_1d(S.st[b].col, col + clo, cb, &S.bar_st[b], pol);
 }
 
-__device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, int me, int nb, int64_t nchunks,
-                                           int CH, double *part_out, PipeState &ps, uint64_t pol) {
+// Chunks handled: cbase + me + k*nb for k = 0.. while < cbase + nloc (cbase =
+// 0, nloc = all chunks on one GPU; the owned chunk range of a partition in
+// the distributed CG).  L.row_ptr is indexed by global row.
+__device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
+                                           int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol) {
     const int tid = threadIdx.x;
     const int64_t n = L.n;
-    const int64_t K = me < nchunks ? (nchunks - 1 - me) / nb + 1 : 0;  // my chunks
+    const int64_t K = me < nloc ? (nloc - 1 - me) / nb + 1 : 0;  // my chunks
     if (K == 0) return;
     const double *p = L.p;  // written by other CTAs in earlier phases: coherent loads
     auto chunk_rows = [&](int64_t k, int64_t &cr0, int &crows) {
-        const int64_t c = me + k * nb;
+        const int64_t c = cbase + me + k * nb;
         cr0 = c * CH * NT;
         crows = (int)(n - cr0 < (int64_t)CH * NT ? n - cr0 : (int64_t)CH * NT);
     };
@@ -397,7 +400,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
         }
         const double s = block_sum<NT>(dot, S.red);  // its barriers also retire rp buffer cs&1
         if (tid == 0) {
-            part_out[me + k * nb] = s;
+            part_out[cbase + me + k * nb] = s;
             if (k + 2 < K) {
                 int64_t nr0;
                 int nrows;
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
             if (it >= L.max_iter) { status = 1; break; }
             tick(-1);
             // ---- q = A p, pq = p.q
-            spmv_phase(S, L, me, nb, nchunks, CH, part + nchunks, ps, pol);
+            spmv_phase(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol);
             tick(0);
             const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, S.red);
             tick(1);
@@ -572,6 +575,159 @@ __global__ void __launch_bounds__(NT) k_spmv(int64_t n, const int64_t *__restric
     spmv_chunk(S, row_ptr, col, val, v, y, r0, nr, 1, phase, J, pol);
 }
 
+// ---------------------------------------------------------------------------
+// Distributed CG (one partition = a contiguous range of whole chunks of one
+// level).  The same arithmetic as k_cg, split into phase kernels so that the
+// chunk partials can be all-reduced (NCCL or the single-process emulation)
+// and the halo of p exchanged between phases.  Scalars live on the device;
+// kernels do nothing once the CG has stopped.  Because every partial is
+// computed per chunk exactly as in k_cg and summed over all chunks in the
+// same fixed order, the result is bit-identical to the single-GPU solve for
+// any number of partitions.
+__device__ __forceinline__ void dcg_check_top(DistCGScalars &s, double tol2, int max_iter) {
+    if (!(s.bb > 0.0) || s.rr <= tol2 * s.bb) {
+        s.active = 0;
+    } else if (s.it >= max_iter) {
+        s.active = 0;
+        s.status = 1;
+    } else {
+        s.active = 1;
+    }
+}
+
+__global__ void __launch_bounds__(NT) k_dcg_init(DistCGArgs A) {
+    __shared__ double red[NT / 32 + 2];
+    const CGLevelArgs &L = A.L;
+    const int CH = L.chunk_tiles, tid = threadIdx.x;
+    for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x) {
+        double acc = 0.0;
+        for (int t = 0; t < CH; ++t) {
+            int64_t i = (c * CH + t) * NT + tid;
+            if (i < L.n) {
+                double bi = L.b_src ? __ldg(&L.b_src[__ldg(&L.b_perm[i])]) : __ldg(&L.b[i]);
+                L.x[i] = 0.0;
+                L.r[i] = bi;
+                L.p[i] = bi;
+                acc += bi * bi;
+            }
+        }
+        double s = block_sum<NT>(acc, red);
+        if (tid == 0) A.part_send[c] = s;
+    }
+}
+
+__global__ void __launch_bounds__(NT, 3) k_dcg_spmv(DistCGArgs A) {
+    if (!A.sc->active) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CGSharedT &S = *reinterpret_cast<CGSharedT *>(smem_raw);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        mbar_init(&S.bar_rp[0], 1);
+        mbar_init(&S.bar_rp[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    PipeState ps{0u, 0u};
+    spmv_phase(S, A.L, blockIdx.x, gridDim.x, A.c0, A.c1 - A.c0, A.L.chunk_tiles, A.part_send, ps,
+               policy_evict_first());
+}
+
+__global__ void __launch_bounds__(NT) k_dcg_rupd(DistCGArgs A) {
+    if (!A.sc->active) return;
+    __shared__ double red[NT / 32 + 2];
+    const CGLevelArgs &L = A.L;
+    const int CH = L.chunk_tiles, tid = threadIdx.x;
+    const double alpha = A.sc->alpha;
+    for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x) {
+        double acc = 0.0;
+        for (int t = 0; t < CH; ++t) {
+            int64_t i = (c * CH + t) * NT + tid;
+            if (i < L.n) {
+                double ri = L.r[i] - alpha * L.q[i];
+                L.r[i] = ri;
+                acc += ri * ri;
+            }
+        }
+        double s = block_sum<NT>(acc, red);
+        if (tid == 0) A.part_send[c] = s;
+    }
+}
+
+__global__ void __launch_bounds__(NT) k_dcg_xpupd(DistCGArgs A) {
+    if (!A.sc->active) return;
+    const CGLevelArgs &L = A.L;
+    const int CH = L.chunk_tiles, tid = threadIdx.x;
+    const double alpha = A.sc->alpha, beta = A.sc->beta;
+    for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x)
+        for (int t = 0; t < CH; ++t) {
+            int64_t i = (c * CH + t) * NT + tid;
+            if (i < L.n) {
+                const double pv = L.p[i];
+                L.x[i] = L.x[i] + alpha * pv;
+                L.p[i] = L.r[i] + beta * pv;
+            }
+        }
+}
+
+// mode 0: after init (bb); 1: after SpMV (pq, alpha); 2: after the r update
+// (rr', beta); 3: end of iteration (it++, stopping test).  One CTA; the sum
+// over chunks uses the order of chunk_allreduce.
+__global__ void __launch_bounds__(NT) k_dcg_scalar(DistCGArgs A, int mode) {
+    __shared__ double red[NT / 32 + 2];
+    DistCGScalars &s = *A.sc;
+    if (mode != 0 && !s.active) return;
+    double v = 0.0;
+    if (mode != 3) {
+        double t = 0.0;
+        for (int64_t j = threadIdx.x; j < A.nchunks; j += NT) t += A.part_recv[j];
+        v = block_sum<NT>(t, red);
+    }
+    if (threadIdx.x != 0) return;
+    if (mode == 0) {
+        s.bb = v;
+        s.rr = v;
+        s.it = 0;
+        s.status = 0;
+        dcg_check_top(s, A.L.tol2, A.L.max_iter);
+    } else if (mode == 1) {
+        s.pq = v;
+        s.alpha = s.rr / v;
+    } else if (mode == 2) {
+        s.beta = v / s.rr;
+        s.rr = v;
+    } else {
+        s.it += 1;
+        dcg_check_top(s, A.L.tol2, A.L.max_iter);
+    }
+}
+
+__global__ void k_sum_arrays(int W, DistPtrs srcs, double *dst, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int w = 0; w < W; ++w) s += srcs.p[w][i];
+    dst[i] = s;
+}
+
+__global__ void k_col_minmax(int64_t nnz, const int32_t *__restrict__ col, unsigned long long *mm) {
+    unsigned long long lo = ~0ull, hi = 0;
+    for (int64_t p = (int64_t)blockIdx.x * NT + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * NT) {
+        unsigned long long c = (unsigned long long)col[p];
+        lo = c < lo ? c : lo;
+        hi = c > hi ? c : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, lo, o);
+        lo = t < lo ? t : lo;
+        t = __shfl_xor_sync(0xffffffffu, hi, o);
+        hi = t > hi ? t : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
 int g_max_resident = 0;
 
 void set_smem_attrs() {
@@ -579,6 +735,7 @@ void set_smem_attrs() {
     if (done) return;
     MSK_CUDA(cudaFuncSetAttribute(k_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGSharedT)));
     MSK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
+    MSK_CUDA(cudaFuncSetAttribute(k_dcg_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGSharedT)));
     done = true;
 }
 }  // namespace
@@ -667,6 +824,52 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     if (launches) *launches += 1;
     MSK_CUDA(cudaFreeAsync(partials, st));
     MSK_CUDA(cudaFreeAsync(bars, st));
+}
+
+namespace {
+unsigned dcg_grid(const DistCGArgs &a, int per_sm) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t nc = a.c1 - a.c0;
+    int64_t g = (int64_t)sms * per_sm;
+    return (unsigned)(nc < 1 ? 1 : (nc < g ? nc : g));
+}
+}  // namespace
+
+void dcg_init(const DistCGArgs &a, cudaStream_t st) {
+    k_dcg_init<<<dcg_grid(a, 8), NT, 0, st>>>(a);
+    MSK_CHECK_LAUNCH();
+}
+void dcg_spmv(const DistCGArgs &a, cudaStream_t st) {
+    set_smem_attrs();
+    k_dcg_spmv<<<dcg_grid(a, 3), NT, sizeof(CGSharedT), st>>>(a);
+    MSK_CHECK_LAUNCH();
+}
+void dcg_rupd(const DistCGArgs &a, cudaStream_t st) {
+    k_dcg_rupd<<<dcg_grid(a, 8), NT, 0, st>>>(a);
+    MSK_CHECK_LAUNCH();
+}
+void dcg_xpupd(const DistCGArgs &a, cudaStream_t st) {
+    k_dcg_xpupd<<<dcg_grid(a, 8), NT, 0, st>>>(a);
+    MSK_CHECK_LAUNCH();
+}
+void dcg_scalar(const DistCGArgs &a, int mode, cudaStream_t st) {
+    k_dcg_scalar<<<1, NT, 0, st>>>(a, mode);
+    MSK_CHECK_LAUNCH();
+}
+void sum_arrays(int W, const DistPtrs &srcs, double *dst, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_sum_arrays<<<ceil_div_u(n, NT), NT, 0, st>>>(W, srcs, dst, n);
+    MSK_CHECK_LAUNCH();
+}
+void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStream_t st) {
+    unsigned long long init[2] = {~0ull, 0ull};
+    MSK_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+    if (nnz <= 0) return;
+    int64_t nb = (nnz + NT - 1) / NT;
+    k_col_minmax<<<(unsigned)(nb < 1184 ? nb : 1184), NT, 0, st>>>(nnz, col, mm);
+    MSK_CHECK_LAUNCH();
 }
 
 void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,

@@ -87,6 +87,32 @@ struct CGLevelArgs {
     int *out_status;          // device: 0 ok, 1 noconv
     unsigned long long *dbg;  // optional: 6 phase times (ns) of CTA 0 (spmv, bar1, r, bar2, p, bar3)
 };
+// ---- distributed CG (partitioned levels; cg.cu)
+constexpr int kMaxParts = 16;
+struct DistCGScalars {
+    double bb, rr, pq, alpha, beta;
+    int it, active, status, pad;
+};
+struct DistCGArgs {
+    CGLevelArgs L;             // n, tol2, max_iter, chunk_tiles, vectors (full length, owned rows
+                               // valid), row_ptr indexed by GLOBAL row (local storage - lo), col/val local
+    int64_t c0, c1, nchunks;   // owned chunks [c0, c1) of nchunks
+    double *part_send;         // nchunks, zero outside the owned chunks
+    const double *part_recv;   // nchunks after the all-reduce
+    DistCGScalars *sc;
+};
+struct DistPtrs {
+    const double *p[kMaxParts];
+};
+int cg_chunk_tiles(int64_t n);
+void dcg_init(const DistCGArgs &a, cudaStream_t st);
+void dcg_spmv(const DistCGArgs &a, cudaStream_t st);
+void dcg_rupd(const DistCGArgs &a, cudaStream_t st);
+void dcg_xpupd(const DistCGArgs &a, cudaStream_t st);
+void dcg_scalar(const DistCGArgs &a, int mode, cudaStream_t st);
+void sum_arrays(int W, const DistPtrs &srcs, double *dst, int64_t n, cudaStream_t st);
+void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStream_t st);
+
 // Run independent CGs on several levels in one cooperative launch.
 // CSR arrays must be 16-byte aligned and padded: row_ptr n+3 entries,
 // col nnz+4, val nnz+2 (bulk copies round their extents to 16 bytes).

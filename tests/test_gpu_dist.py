@@ -1,0 +1,80 @@
+"""Partitioned (multi-GPU) path, run as the single-process emulation on one
+GPU: `world` partitions per level, chunk partials all-reduced, p halos
+exchanged between separate partition buffers.
+
+Because every partial is formed per chunk exactly as in the single-GPU
+kernel and summed over all chunks in the same order, the partitioned solve
+must reproduce the single-GPU alpha and s_L BIT FOR BIT for any world size.
+The oracle bar (1e-9 per level) then carries over.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import config, halton_hierarchy, uniform_points
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def msk():
+    import paper_2503_04914_b200 as m
+    m.load()
+    return m
+
+
+HIERS = {
+    "C1": lambda: config("C1", m_eval=0),
+    "halton3d": lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5),
+    "C3P4": lambda: config("C3P4", m_eval=0),
+}
+
+
+def _solve(msk, ctx, H, flags, f, x):
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=flags)
+    h.assemble()
+    a, info = h.solve(f, tol=1e-12)
+    s, einfo = h.evaluate(x)
+    return a, s, info, einfo
+
+
+@pytest.mark.parametrize("name", list(HIERS))
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_partitioned_equals_single_gpu_bitwise(msk, name, world):
+    H = HIERS[name]()
+    f = H.f()
+    x = uniform_points(5000, H.d, seed=4)
+    c1 = msk.Context(0)
+    a1, s1, i1, e1 = _solve(msk, c1, H, 0, f, x)
+    cw = msk.Context(0, rank=-1, world=world)
+    aw, sw, iw, ew = _solve(msk, cw, H, msk.MSK_FLAG_DIST_ALL, f, x)
+    for l in range(H.L):
+        assert np.array_equal(aw[l], a1[l]), (name, world, l, np.abs(aw[l] - a1[l]).max())
+        assert iw.cg_iters[l] == i1.cg_iters[l]
+    assert np.array_equal(sw, s1)
+    assert ew.nnz == e1.nnz
+    c1.close()
+    cw.close()
+
+
+def test_partitioned_matches_oracle_and_default_threshold(msk):
+    """C3 4-level prefix: with the default threshold (>= 2^20 points) no level
+    is partitioned; with DIST_ALL every level with >= world chunks is.  Both
+    match the oracle within the 1e-9 bar."""
+    H = config("C3P4", m_eval=0)
+    f = H.f()
+    cw = msk.Context(0, rank=-1, world=4)
+    for flags in (0, msk.MSK_FLAG_DIST_ALL):
+        h = msk.Hierarchy(cw, H.points, H.delta, H.q, k=1, flags=flags)
+        h.assemble()
+        a, _ = h.solve(f)
+        ao, _, _ = oracle.sequential(H.points, H.delta, f, tol=1e-12, direct_max_n=0)
+        for l in range(H.L):
+            assert np.linalg.norm(a[l] - ao[l]) <= 1e-9 * np.linalg.norm(ao[l])
+    with pytest.raises(msk.MskError) as ei:
+        h.solve(f, schedule="literal")
+    assert ei.value.status == 1
+    with pytest.raises(msk.MskError) as ei:
+        h.cg_level(3, f[3])
+    assert ei.value.status == 6
+    cw.close()
