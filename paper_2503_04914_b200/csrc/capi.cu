@@ -817,9 +817,11 @@ CGLevelArgs cg_args(msk_hierarchy *h, int l, double tol, int max_iter, const dou
 
 double cg_bytes(const LevelData &D, int iters) {
     // algorithmic bytes: per iteration 12 B/nnz (val + col)
-    // + 88 B/row (row_ptr 8, gathered p 8, q write 8, r-phase 24, x/p-phase 40);
-    // init 32 B/row (b read; x, r, p written)
-    return (double)iters * (12.0 * (double)D.nnz + 88.0 * (double)D.n) + 32.0 * (double)D.n;
+    // + 88 B/row (SpMV pass: row_ptr 8, gathered r 8, p/q/x read + write 48;
+    // r pass: r, q read + r write 24); iteration 0 reads no p/q/x (-24 B/row);
+    // init 16 B/row (b read, r write); final x update 24 B/row (x, p read, x write)
+    if (iters <= 0) return 24.0 * (double)D.n;
+    return (double)iters * (12.0 * (double)D.nnz + 88.0 * (double)D.n) + 16.0 * (double)D.n;
 }
 
 }  // namespace
@@ -903,7 +905,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
 
     // ---- distributed solve of one partitioned level:
     // beta on the owned rows, then the CG as phase kernels with all-reduced
-    // chunk partials and halo exchange of p; alpha assembled on every rank.
+    // chunk partials and halo exchange of r; alpha assembled on every rank.
     auto dist_level = [&](int l, double tl) {
         auto &Dd = h->dist[l];
         LevelData &D = h->lev[l];
@@ -988,17 +990,17 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 for (int i = 0; i < np; ++i)
                     for (int s = 0; s < W; ++s)
                         if (rl[i][s] < rh[i][s])
-                            MSK_CUDA(cudaMemcpyAsync(Pv[i] + rl[i][s], Pv[s] + rl[i][s],
+                            MSK_CUDA(cudaMemcpyAsync(R[i] + rl[i][s], R[s] + rl[i][s],
                                                      sizeof(double) * (size_t)(rh[i][s] - rl[i][s]),
                                                      cudaMemcpyDeviceToDevice, st));
             } else {
                 MSK_NCCL(nccl_api()->GroupStart());
                 for (int s = 0; s < W; ++s) {
                     if (sl[0][s] < sh[0][s])
-                        MSK_NCCL(nccl_api()->Send(Pv[0] + sl[0][s], (size_t)(sh[0][s] - sl[0][s]), ncclFloat64, s,
+                        MSK_NCCL(nccl_api()->Send(R[0] + sl[0][s], (size_t)(sh[0][s] - sl[0][s]), ncclFloat64, s,
                                                   h->ctx->comm, st));
                     if (rl[0][s] < rh[0][s])
-                        MSK_NCCL(nccl_api()->Recv(Pv[0] + rl[0][s], (size_t)(rh[0][s] - rl[0][s]), ncclFloat64, s,
+                        MSK_NCCL(nccl_api()->Recv(R[0] + rl[0][s], (size_t)(rh[0][s] - rl[0][s]), ncclFloat64, s,
                                                   h->ctx->comm, st));
                 }
                 MSK_NCCL(nccl_api()->GroupEnd());
@@ -1018,10 +1020,9 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 for (int i = 0; i < np; ++i) dcg_rupd(args[i], st);
                 allreduce();
                 for (int i = 0; i < np; ++i) dcg_scalar(args[i], 2, st);
-                for (int i = 0; i < np; ++i) dcg_xpupd(args[i], st);
                 for (int i = 0; i < np; ++i) dcg_scalar(args[i], 3, st);
                 halo();
-                launches += 7 * np + (emu ? 2 : 0);
+                launches += 6 * np + (emu ? 2 : 0);
             }
             done += 8;
             DistCGScalars hs;
@@ -1029,6 +1030,8 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             MSK_CUDA(cudaStreamSynchronize(st));
             if (!hs.active || done > max_iter + 16) break;
         }
+        for (int i = 0; i < np; ++i) dcg_xfin(args[i], st);
+        launches += np;
         cg_t.back()->stop();
         // alpha^(l) complete on every rank (spatial order), then caller order
         if (emu) {

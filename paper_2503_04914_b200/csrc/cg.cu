@@ -8,21 +8,29 @@
 // with its own device-side barrier and deterministic reductions, so the whole
 // solve of all levels is one launch with no host round trips:
 //
-//   x = 0, r = b, p = b, bb = rr = b.b
+//   x = 0, r = b, bb = rr = b.b, beta = alpha' = 0
 //   while rr > tol^2 bb and it < max_iter:          (reading C-9)
-//       q = A p ; pq = p.q            -- SpMV fused with the dot      [barrier]
+//       w = A r ; p = r + beta p ; q = w + beta q ; x += alpha' p_old ;
+//       pq = p.q                     -- ONE pass: SpMV + updates + dot [barrier]
 //       alpha = rr / pq
 //       r -= alpha q ; rr' = r.r      -- fused update + dot           [barrier]
-//       beta = rr' / rr
-//       x += alpha p ; p = r + beta p -- x update deferred to here    [barrier]
+//       beta = rr' / rr ; alpha' = alpha
+//   x += alpha' p                     -- the last deferred x update
+//
+// This is Algorithm 1's CG with q = A p formed by the
+// recurrence q = A r + beta q (A p = A r + beta A p_old), which lets the
+// x/p update ride on the SpMV pass: two device-wide barriers per iteration
+// instead of three, the same 88 bytes of vector traffic per row.  In exact
+// arithmetic the iterates are those of the textbook loop; in floating point
+// they differ by rounding only (parity: tests/test_gpu_parity.py).
 //
 // SpMV: a CTA takes a tile of NT consecutive rows (spatial order).  One
 // thread streams the tile's contiguous CSR slices (values, columns) into
 // shared memory with a bulk-async copy (TMA, cp.async.bulk, L2 evict-first
-// so the gathered vector p stays L2-resident) completing on an mbarrier; the
-// threads then only issue the irregular gathers p[col] (8 independent loads
-// in flight per thread), multiply in place, and each thread sums its row in
-// ascending column order (deterministic).
+// so the gathered vector r stays L2-resident) completing on an mbarrier; the
+// threads then only issue the irregular gathers r[col] (U independent loads
+// in flight per thread), and each thread sums its row in ascending column
+// order (deterministic).
 //
 // Work unit and reductions: a level's tiles are grouped into chunks of CH
 // tiles (CH fixed by n alone); chunk c belongs to CTA c mod nb.  Each chunk
@@ -263,8 +271,9 @@ __device__ __forceinline__ double spmv_chunk(CGShared &S, const int64_t *row_ptr
 }
 
 // ---------------------------------------------------------------------------
-// CTA-level pipelined SpMV phase: q = A p over all chunks of this CTA, with
-// pq partials per chunk.  The CTA's CSR entries are streamed as a sequence of
+// CTA-level pipelined SpMV phase over all chunks of this CTA: w = A r, then
+// per row p = r + beta p, q = w + beta q, x += alpha' p_old (first iteration:
+// p = r, q = w, x = 0), with p.q partials per chunk.  The CTA's CSR entries are streamed as a sequence of
 // pieces (<= CAPTE entries, two bulk copies each) through two stages: piece
 // P+1 is in flight while piece P is consumed.  Row pointers of the next chunk
 // are prefetched into the second rp buffer.  Each thread owns row
@@ -299,12 +308,13 @@ __device__ __forceinline__ void issue_piece_t(CGSharedT &S, int b, const int32_t
 // 0, nloc = all chunks on one GPU; the owned chunk range of a partition in
 // the distributed CG).  L.row_ptr is indexed by global row.
 __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
-                                           int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol) {
+                                           int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol,
+                                           bool first, double alpha_prev, double beta) {
     const int tid = threadIdx.x;
     const int64_t n = L.n;
     const int64_t K = me < nloc ? (nloc - 1 - me) / nb + 1 : 0;  // my chunks
     if (K == 0) return;
-    const double *p = L.p;  // written by other CTAs in earlier phases: coherent loads
+    const double *rv = L.r;  // written by other CTAs in the previous phase (after the barrier)
     auto chunk_rows = [&](int64_t k, int64_t &cr0, int &crows) {
         const int64_t c = cbase + me + k * nb;
         cr0 = c * CH * NT;
@@ -376,7 +386,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int ee = e + u;
-                        pv[u] = ee < hi ? p[cur.col[coff + ee]] : 0.0;
+                        pv[u] = ee < hi ? rv[cur.col[coff + ee]] : 0.0;
                         vv[u] = ee < hi ? cur.val[voff + ee] : 0.0;
                     }
 #pragma unroll
@@ -389,13 +399,33 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
             kb = ke;
         }
         double dot = 0.0;
+        {
+            double *__restrict__ x = L.x;
+            double *__restrict__ p = L.p;
+            double *__restrict__ q = L.q;
+            double ri[MAXCH], po[MAXCH], qo[MAXCH], xo[MAXCH];
 #pragma unroll
-        for (int t = 0; t < MAXCH; ++t) {
-            const int r = t * NT + tid;
-            if (t < CH && r < crows) {
+            for (int t = 0; t < MAXCH; ++t) {
+                const int r = t * NT + tid;
+                const bool ok = t < CH && r < crows;
                 const int64_t i = cr0 + r;
-                L.q[i] = acc[t];
-                dot += p[i] * acc[t];
+                ri[t] = ok ? rv[i] : 0.0;
+                po[t] = ok && !first ? p[i] : 0.0;
+                qo[t] = ok && !first ? q[i] : 0.0;
+                xo[t] = ok && !first ? x[i] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < MAXCH; ++t) {
+                const int r = t * NT + tid;
+                if (t < CH && r < crows) {
+                    const int64_t i = cr0 + r;
+                    const double pn = first ? ri[t] : ri[t] + beta * po[t];
+                    const double qn = first ? acc[t] : acc[t] + beta * qo[t];
+                    p[i] = pn;
+                    q[i] = qn;
+                    x[i] = first ? 0.0 : xo[t] + alpha_prev * po[t];
+                    dot += pn * qn;
+                }
             }
         }
         const double s = block_sum<NT>(dot, S.red);  // its barriers also retire rp buffer cs&1
@@ -437,16 +467,14 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
     __syncthreads();
     const uint64_t pol = policy_evict_first();
 
-    // ---- init: x = 0, r = p = b, bb = b.b
+    // ---- init: r = b, bb = b.b (x, p, q are first written by iteration 0)
     for (int64_t c = me; c < nchunks; c += nb) {
         double acc = 0.0;
         for (int t = 0; t < CH; ++t) {
             int64_t i = (c * CH + t) * NT + tid;
             if (i < n) {
                 double bi = L.b_src ? __ldg(&L.b_src[__ldg(&L.b_perm[i])]) : __ldg(&L.b[i]);
-                L.x[i] = 0.0;
                 L.r[i] = bi;
-                L.p[i] = bi;
                 acc += bi * bi;
             }
         }
@@ -467,18 +495,19 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
             tprev = now;
         }
     };
+    double alpha = 0.0, beta = 0.0;
     if (bb > 0.0) {
         const double stop = L.tol2 * bb;
         for (;;) {
             if (rr <= stop) break;
             if (it >= L.max_iter) { status = 1; break; }
             tick(-1);
-            // ---- q = A p, pq = p.q
-            spmv_phase(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol);
+            // ---- w = A r ; p = r + beta p ; q = w + beta q ; x += alpha p_old ; pq = p.q
+            spmv_phase(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol, it == 0, alpha, beta);
             tick(0);
             const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, S.red);
             tick(1);
-            const double alpha = rr / pq;
+            alpha = rr / pq;
             // ---- r -= alpha q, rr' = r.r
             {
                 double *__restrict__ r = L.r;
@@ -509,48 +538,23 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
             tick(2);
             const double rrn = chunk_allreduce(part + 2 * nchunks, nchunks, nb, L.barrier, round, S.red);
             tick(3);
-            const double beta = rrn / rr;
+            beta = rrn / rr;
             rr = rrn;
-            // ---- x += alpha p, p = r + beta p
-            {
-                double *__restrict__ x = L.x;
-                double *__restrict__ p = L.p;
-                const double *__restrict__ r = L.r;
-                for (int64_t c = me; c < nchunks; c += nb) {
-                    double xv[MAXCH], pv[MAXCH], rv[MAXCH];
-#pragma unroll
-                    for (int t = 0; t < MAXCH; ++t) {
-                        int64_t i = (c * CH + t) * NT + tid;
-                        bool ok = t < CH && i < n;
-                        xv[t] = ok ? x[i] : 0.0;
-                        pv[t] = ok ? p[i] : 0.0;
-                        rv[t] = ok ? r[i] : 0.0;
-                    }
-#pragma unroll
-                    for (int t = 0; t < MAXCH; ++t) {
-                        int64_t i = (c * CH + t) * NT + tid;
-                        if (t < CH && i < n) {
-                            x[i] = xv[t] + alpha * pv[t];
-                            p[i] = rv[t] + beta * pv[t];
-                        }
-                    }
-                }
-            }
-            tick(4);
-            group_barrier(L.barrier, nb, round);
-            tick(5);
             ++it;
         }
     }
     if (tdbg)
         for (int k = 0; k < 6; ++k) L.dbg[k] = tph[k];
-    if (L.x_out) {
-        for (int64_t c = me; c < nchunks; c += nb)
-            for (int t = 0; t < CH; ++t) {
-                int64_t i = (c * CH + t) * NT + tid;
-                if (i < n) L.x_out[__ldg(&L.x_perm[i])] = L.x[i];
+    // ---- the last deferred update x += alpha p (own rows: no barrier needed)
+    for (int64_t c = me; c < nchunks; c += nb)
+        for (int t = 0; t < CH; ++t) {
+            int64_t i = (c * CH + t) * NT + tid;
+            if (i < n) {
+                const double xi = it > 0 ? L.x[i] + alpha * L.p[i] : 0.0;
+                L.x[i] = xi;
+                if (L.x_out) L.x_out[__ldg(&L.x_perm[i])] = xi;
             }
-    }
+        }
     if (me == 0 && tid == 0) {
         *L.out_iters = it;
         L.out_rr[0] = rr;
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(NT) k_spmv(int64_t n, const int64_t *__restric
 // Distributed CG (one partition = a contiguous range of whole chunks of one
 // level).  The same arithmetic as k_cg, split into phase kernels so that the
 // chunk partials can be all-reduced (NCCL or the single-process emulation)
-// and the halo of p exchanged between phases.  Scalars live on the device;
+// and the halo of r exchanged between phases.  Scalars live on the device;
 // kernels do nothing once the CG has stopped.  Because every partial is
 // computed per chunk exactly as in k_cg and summed over all chunks in the
 // same fixed order, the result is bit-identical to the single-GPU solve for
@@ -605,9 +609,7 @@ __global__ void __launch_bounds__(NT) k_dcg_init(DistCGArgs A) {
             int64_t i = (c * CH + t) * NT + tid;
             if (i < L.n) {
                 double bi = L.b_src ? __ldg(&L.b_src[__ldg(&L.b_perm[i])]) : __ldg(&L.b[i]);
-                L.x[i] = 0.0;
                 L.r[i] = bi;
-                L.p[i] = bi;
                 acc += bi * bi;
             }
         }
@@ -628,8 +630,9 @@ __global__ void __launch_bounds__(NT, 3) k_dcg_spmv(DistCGArgs A) {
     }
     __syncthreads();
     PipeState ps{0u, 0u};
+    const DistCGScalars &sc = *A.sc;
     spmv_phase(S, A.L, blockIdx.x, gridDim.x, A.c0, A.c1 - A.c0, A.L.chunk_tiles, A.part_send, ps,
-               policy_evict_first());
+               policy_evict_first(), sc.it == 0, sc.alpha, sc.beta);
 }
 
 __global__ void __launch_bounds__(NT) k_dcg_rupd(DistCGArgs A) {
@@ -653,19 +656,17 @@ __global__ void __launch_bounds__(NT) k_dcg_rupd(DistCGArgs A) {
     }
 }
 
-__global__ void __launch_bounds__(NT) k_dcg_xpupd(DistCGArgs A) {
-    if (!A.sc->active) return;
+// after the loop: the last deferred x += alpha p on the owned rows (x = 0
+// when no iteration ran)
+__global__ void __launch_bounds__(NT) k_dcg_xfin(DistCGArgs A) {
     const CGLevelArgs &L = A.L;
     const int CH = L.chunk_tiles, tid = threadIdx.x;
-    const double alpha = A.sc->alpha, beta = A.sc->beta;
+    const bool any = A.sc->it > 0;
+    const double alpha = A.sc->alpha;
     for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x)
         for (int t = 0; t < CH; ++t) {
             int64_t i = (c * CH + t) * NT + tid;
-            if (i < L.n) {
-                const double pv = L.p[i];
-                L.x[i] = L.x[i] + alpha * pv;
-                L.p[i] = L.r[i] + beta * pv;
-            }
+            if (i < L.n) L.x[i] = any ? L.x[i] + alpha * L.p[i] : 0.0;
         }
 }
 
@@ -686,6 +687,8 @@ __global__ void __launch_bounds__(NT) k_dcg_scalar(DistCGArgs A, int mode) {
     if (mode == 0) {
         s.bb = v;
         s.rr = v;
+        s.alpha = 0.0;
+        s.beta = 0.0;
         s.it = 0;
         s.status = 0;
         dcg_check_top(s, A.L.tol2, A.L.max_iter);
@@ -850,8 +853,8 @@ void dcg_rupd(const DistCGArgs &a, cudaStream_t st) {
     k_dcg_rupd<<<dcg_grid(a, 8), NT, 0, st>>>(a);
     MSK_CHECK_LAUNCH();
 }
-void dcg_xpupd(const DistCGArgs &a, cudaStream_t st) {
-    k_dcg_xpupd<<<dcg_grid(a, 8), NT, 0, st>>>(a);
+void dcg_xfin(const DistCGArgs &a, cudaStream_t st) {
+    k_dcg_xfin<<<dcg_grid(a, 8), NT, 0, st>>>(a);
     MSK_CHECK_LAUNCH();
 }
 void dcg_scalar(const DistCGArgs &a, int mode, cudaStream_t st) {

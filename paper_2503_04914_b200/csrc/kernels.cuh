@@ -108,7 +108,7 @@ int cg_chunk_tiles(int64_t n);
 void dcg_init(const DistCGArgs &a, cudaStream_t st);
 void dcg_spmv(const DistCGArgs &a, cudaStream_t st);
 void dcg_rupd(const DistCGArgs &a, cudaStream_t st);
-void dcg_xpupd(const DistCGArgs &a, cudaStream_t st);
+void dcg_xfin(const DistCGArgs &a, cudaStream_t st);
 void dcg_scalar(const DistCGArgs &a, int mode, cudaStream_t st);
 void sum_arrays(int W, const DistPtrs &srcs, double *dst, int64_t n, cudaStream_t st);
 void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStream_t st);

@@ -1,5 +1,5 @@
 """Partitioned (multi-GPU) path, run as the single-process emulation on one
-GPU: `world` partitions per level, chunk partials all-reduced, p halos
+GPU: `world` partitions per level, chunk partials all-reduced, r halos
 exchanged between separate partition buffers.
 
 Because every partial is formed per chunk exactly as in the single-GPU

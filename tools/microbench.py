@@ -18,6 +18,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--eval", action="store_true",
+                    help="only time s_L at 1e7 uniform points (first k_gather launch = evaluation)")
     args = ap.parse_args()
     import torch
     import paper_2503_04914_b200 as msk
@@ -28,6 +30,19 @@ def main():
     h = msk.Hierarchy(ctx, [torch.from_numpy(p).to(dev) for p in H.points], H.delta, H.q, k=H.k)
     h.assemble()
     info = h.info()
+    if args.eval:
+        from workloads import uniform_points
+        f = H.f()
+        h.solve(f)
+        x = torch.from_numpy(uniform_points(10_000_000, H.d, seed=7)).to(dev)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()  # ncu --profile-from-start off captures from here
+        ts = []
+        for _ in range(args.reps + 1):
+            _, einfo = h.evaluate(x)
+            ts.append(einfo.t_eval_ms)
+        print(json.dumps({"config": args.config, "m": 10_000_000, "eval_kernel_ms": ts[1:]}))
+        return
     L = H.L
     lf = L - 1
     n, nnz = H.n[lf], int(info.nnz_A[lf])
@@ -51,7 +66,7 @@ def main():
         its.append(it)
     t = ts[-1]
     it = its[-1]
-    cgb = it * (12.0 * nnz + 88.0 * n) + 32.0 * n
+    cgb = it * (12.0 * nnz + 88.0 * n) + 16.0 * n   # DESIGN.md §7 (k_cg algorithmic bytes)
     out.update(cg_ms=t, cg_iters=it, cg_ms_per_iter=t / max(it, 1), cg_GBs=cgb / (t * 1e-3) / 1e9)
     if L > 1:
         vc = torch.rand(H.n[lf - 1], dtype=torch.float64, device=dev)
