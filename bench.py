@@ -242,6 +242,7 @@ def run_msk(args, rank, world, local_rank):
                    "config": args.config, "schedule": sched, "tol": args.tol, "threshold_T": thr,
                    "n_per_level": H.n, "nnz_A": [int(hinfo.nnz_A[l]) for l in range(L)],
                    "cg_iters": [int(sinfo.cg_iters[l]) for l in range(L)],
+                   "kappa_est": [round(float(sinfo.kappa_est[l]), 2) for l in range(L)],
                    "m_eval": int(H.eval_points.shape[0]),
                    "nnz_per_step": nnz_local,
                    "l2": "inputs (274 MB points, 240 MB eval points) larger than the 126 MB L2, plus a 256 MB flush write between steps",

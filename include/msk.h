@@ -99,6 +99,10 @@ typedef struct {
     double t_cg_level_ms[MSK_MAX_LEVELS];   /* device time of the CG launch(es) per level       */
     double bytes_cg_level[MSK_MAX_LEVELS];  /* algorithmic bytes of those launches              */
     int32_t launches;                       /* kernels launched by the call                     */
+    double kappa_est[MSK_MAX_LEVELS];       /* condition number of A_l estimated from the CG
+                                               coefficients of the solve that produced alpha_l
+                                               (extreme eigenvalues of the Lanczos tridiagonal,
+                                               Sturm bisection on the host); 0 if no iteration */
 } msk_solve_info;
 
 /* Per-hierarchy facts (msk_hierarchy_info). */

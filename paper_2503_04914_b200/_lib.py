@@ -31,7 +31,7 @@ class SolveInfo(ctypes.Structure):
                 ("nnz_cg", _dbl), ("nnz_gather", _dbl), ("bytes_cg", _dbl),
                 ("t_cg_ms", _dbl), ("t_gather_ms", _dbl), ("t_total_ms", _dbl),
                 ("t_cg_level_ms", _dbl * MSK_MAX_LEVELS), ("bytes_cg_level", _dbl * MSK_MAX_LEVELS),
-                ("launches", _i32)]
+                ("launches", _i32), ("kappa_est", _dbl * MSK_MAX_LEVELS)]
 
 
 class HierarchyInfo(ctypes.Structure):

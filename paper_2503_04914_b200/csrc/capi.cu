@@ -815,6 +815,46 @@ CGLevelArgs cg_args(msk_hierarchy *h, int l, double tol, int max_iter, const dou
     return a;
 }
 
+// Condition number estimate from m CG steps (the Lanczos connection):
+// T = tridiag with T00 = 1/a0, Tjj = 1/aj + b(j-1)/a(j-1), T(j,j+1) = sqrt(bj)/aj;
+// its extreme eigenvalues (Sturm-sequence bisection) approximate those of A.
+double lanczos_kappa(const double *coef, int m) {
+    if (m <= 0) return 0.0;
+    std::vector<double> dg(m), off(m > 1 ? m - 1 : 1, 0.0);
+    for (int j = 0; j < m; ++j) {
+        const double a = coef[2 * j];
+        dg[j] = 1.0 / a + (j > 0 ? coef[2 * j - 1] / coef[2 * j - 2] : 0.0);
+        if (j + 1 < m) off[j] = std::sqrt(std::max(coef[2 * j + 1], 0.0)) / a;
+    }
+    double lo = dg[0], hi = dg[0];
+    for (int j = 0; j < m; ++j) {
+        const double r = (j > 0 ? std::fabs(off[j - 1]) : 0.0) + (j + 1 < m ? std::fabs(off[j]) : 0.0);
+        lo = std::min(lo, dg[j] - r);
+        hi = std::max(hi, dg[j] + r);
+    }
+    auto below = [&](double x) {  // number of eigenvalues < x
+        int c = 0;
+        double q = dg[0] - x;
+        if (q < 0) ++c;
+        for (int j = 1; j < m; ++j) {
+            if (q == 0.0) q = 1e-300;
+            q = dg[j] - x - off[j - 1] * off[j - 1] / q;
+            if (q < 0) ++c;
+        }
+        return c;
+    };
+    auto bisect = [&](int k) {  // the k-th smallest eigenvalue (k = 1..m)
+        double a = lo, b = hi;
+        for (int it = 0; it < 200 && b - a > 1e-15 * std::max(std::fabs(a), std::fabs(b)); ++it) {
+            const double mid = 0.5 * (a + b);
+            if (below(mid) >= k) b = mid; else a = mid;
+        }
+        return 0.5 * (a + b);
+    };
+    const double lmin = bisect(1), lmax = bisect(m);
+    return lmin > 0.0 ? lmax / lmin : 0.0;
+}
+
 double cg_bytes(const LevelData &D, int iters) {
     // algorithmic bytes: per iteration 12 B/nnz (val + col)
     // + 88 B/row (SpMV pass: row_ptr 8, gathered r 8, p/q/x read + write 48;
@@ -860,6 +900,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     MSK_CUDA(cudaMemsetAsync(d_it, 0, sizeof(int) * nslots * L, st));
     MSK_CUDA(cudaMemsetAsync(d_stat, 0, sizeof(int) * nslots * L, st));
     MSK_CUDA(cudaMemsetAsync(d_rr, 0, sizeof(double) * 2 * nslots * L, st));
+    const int coef_cap = std::min(max_iter, 4096);
+    double *d_coef = dalloc<double>((size_t)(2 * coef_cap) * nslots * L, st);
+    auto set_coef = [&](CGLevelArgs &a, int idx) {
+        a.coef = d_coef + (size_t)(2 * coef_cap) * idx;
+        a.coef_cap = coef_cap;
+    };
     unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
     MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
 
@@ -969,6 +1015,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             A.part_send = send[i];
             A.part_recv = recv;
             A.sc = sc + i;
+            if (i == 0) set_coef(A.L, l);
         }
         auto allreduce = [&]() {
             if (emu) {
@@ -1093,9 +1140,11 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             beta = cur;
         }
         std::vector<CGLevelArgs> a;
-        for (int l = 0; l < L; ++l)
+        for (int l = 0; l < L; ++l) {
             a.push_back(cg_args(h, l, tol, max_iter, beta + h->off[l], nullptr, alpha_sp[l], ad[l].ptr,
                                 d_it + l, d_rr + 2 * l, d_stat + l));
+            set_coef(a.back(), l);
+        }
         time_cg(-1);
         cg_batched(a.data(), L, st, &launches);
         cg_t.back()->stop();
@@ -1116,10 +1165,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             if (l == 0) {
                 a = cg_args(h, l, tl, max_iter, nullptr, fd[0].ptr, alpha_sp[l], ad[l].ptr,
                             d_it + l, d_rr + 2 * l, d_stat + l);
+                set_coef(a, l);
             } else {
                 b_products(l, alpha_sp.data(), h->ws_beta(l));
                 a = cg_args(h, l, tl, max_iter, h->ws_beta(l), nullptr, alpha_sp[l], ad[l].ptr,
                             d_it + l, d_rr + 2 * l, d_stat + l);
+                set_coef(a, l);
             }
             debug_sync(st, "b_products");
             time_cg(l);
@@ -1138,9 +1189,11 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         for (int sweep = 0; sweep < L; ++sweep) {
             if (L > 1) {
                 std::vector<CGLevelArgs> a;
-                for (int l = 0; l + 1 < L; ++l)
+                for (int l = 0; l + 1 < L; ++l) {
                     a.push_back(cg_args(h, l, inner_tol, max_iter, h->ws_beta(l), nullptr, t_sp[l], nullptr,
                                         d_it + sweep * L + l, d_rr + 2 * (sweep * L + l), d_stat + sweep * L + l));
+                    set_coef(a.back(), sweep * L + l);
+                }
                 time_cg(-1);
                 cg_batched(a.data(), (int)a.size(), st, &launches);
                 cg_t.back()->stop();
@@ -1149,9 +1202,11 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             }
         }
         std::vector<CGLevelArgs> a;
-        for (int l = 0; l < L; ++l)
+        for (int l = 0; l < L; ++l) {
             a.push_back(cg_args(h, l, tol, max_iter, h->ws_beta(l), nullptr, alpha_sp[l], ad[l].ptr,
                                 d_it + L * L + l, d_rr + 2 * (L * L + l), d_stat + L * L + l));
+            set_coef(a.back(), L * L + l);
+        }
         time_cg(-1);
         cg_batched(a.data(), L, st, &launches);
         cg_t.back()->stop();
@@ -1165,8 +1220,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     MSK_CUDA(cudaMemcpyAsync(stat.data(), d_stat, sizeof(int) * stat.size(), cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * rr.size(), cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaMemcpyAsync(&hits, d_hits, sizeof hits, cudaMemcpyDeviceToHost, st));
+    const int fin_slot = schedule == MSK_SCHED_LITERAL && !thresholded ? L : 0;
+    std::vector<double> coefs((size_t)(2 * coef_cap) * L);
+    MSK_CUDA(cudaMemcpyAsync(coefs.data(), d_coef + (size_t)(2 * coef_cap) * fin_slot * L,
+                             sizeof(double) * coefs.size(), cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaStreamSynchronize(st));
-    dfree(d_it, st); dfree(d_stat, st); dfree(d_rr, st); dfree(d_hits, st);
+    dfree(d_it, st); dfree(d_stat, st); dfree(d_rr, st); dfree(d_hits, st); dfree(d_coef, st);
 
     msk_solve_info loc;
     memset(&loc, 0, sizeof loc);
@@ -1190,6 +1249,8 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             loc.bytes_cg += cg_bytes(h->lev[l], it[idx]);
             if (s == fin) {
                 loc.cg_iters[l] = it[idx];
+                loc.kappa_est[l] = lanczos_kappa(coefs.data() + (size_t)(2 * coef_cap) * l,
+                                                 std::min(it[idx], coef_cap));
                 loc.rel_res[l] = rr[2 * idx + 1] > 0 ? sqrt(rr[2 * idx] / rr[2 * idx + 1]) : 0.0;
                 loc.bytes_cg_level[l] += cg_bytes(h->lev[l], it[idx]);
             } else {
@@ -1512,8 +1573,8 @@ extern "C" msk_status msk_cg_level(msk_hierarchy *h, int level, const double *b,
         unsigned long long hd[6];
         MSK_CUDA(cudaMemcpyAsync(hd, dbg, sizeof hd, cudaMemcpyDeviceToHost, st));
         MSK_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "[msk] cg phases (ms, CTA 0): spmv %.3f bar1 %.3f rupd %.3f bar2 %.3f pupd %.3f bar3 %.3f\n",
-                hd[0] * 1e-6, hd[1] * 1e-6, hd[2] * 1e-6, hd[3] * 1e-6, hd[4] * 1e-6, hd[5] * 1e-6);
+        fprintf(stderr, "[msk] cg phases (ms, CTA 0): spmv+update %.3f bar1 %.3f r-update %.3f bar2 %.3f\n",
+                hd[0] * 1e-6, hd[1] * 1e-6, hd[2] * 1e-6, hd[3] * 1e-6);
         dfree(dbg, st);
     }
     int hit[2];

@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
             const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, S.red);
             tick(1);
             alpha = rr / pq;
+            if (L.coef && me == 0 && tid == 0 && it < L.coef_cap) L.coef[2 * it] = alpha;
             // ---- r -= alpha q, rr' = r.r
             {
                 double *__restrict__ r = L.r;
@@ -540,6 +541,7 @@ __global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
             tick(3);
             beta = rrn / rr;
             rr = rrn;
+            if (L.coef && me == 0 && tid == 0 && it < L.coef_cap) L.coef[2 * it + 1] = beta;
             ++it;
         }
     }
@@ -695,9 +697,11 @@ __global__ void __launch_bounds__(NT) k_dcg_scalar(DistCGArgs A, int mode) {
     } else if (mode == 1) {
         s.pq = v;
         s.alpha = s.rr / v;
+        if (A.L.coef && s.it < A.L.coef_cap) A.L.coef[2 * s.it] = s.alpha;
     } else if (mode == 2) {
         s.beta = v / s.rr;
         s.rr = v;
+        if (A.L.coef && s.it < A.L.coef_cap) A.L.coef[2 * s.it + 1] = s.beta;
     } else {
         s.it += 1;
         dcg_check_top(s, A.L.tol2, A.L.max_iter);

@@ -85,7 +85,9 @@ struct CGLevelArgs {
     int *out_iters;           // device
     double *out_rr;           // device: final rr, bb
     int *out_status;          // device: 0 ok, 1 noconv
-    unsigned long long *dbg;  // optional: 6 phase times (ns) of CTA 0 (spmv, bar1, r, bar2, p, bar3)
+    unsigned long long *dbg;  // optional: 6 phase times (ns) of CTA 0 (spmv, bar1, r, bar2, -, -)
+    double *coef;             // optional: CG scalars (alpha_k, beta_k) of iterations k < coef_cap
+    int coef_cap;             //   (Lanczos tridiagonal -> kappa estimate, msk_solve_info.kappa_est)
 };
 // ---- distributed CG (partitioned levels; cg.cu)
 constexpr int kMaxParts = 16;

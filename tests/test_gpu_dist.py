@@ -51,6 +51,7 @@ def test_partitioned_equals_single_gpu_bitwise(msk, name, world):
     for l in range(H.L):
         assert np.array_equal(aw[l], a1[l]), (name, world, l, np.abs(aw[l] - a1[l]).max())
         assert iw.cg_iters[l] == i1.cg_iters[l]
+        assert iw.kappa_est[l] == i1.kappa_est[l]
     assert np.array_equal(sw, s1)
     assert ew.nnz == e1.nnz
     c1.close()

@@ -167,6 +167,27 @@ def test_cg_zero_rhs_and_noconv(msk, ctx):
     assert ei.value.status == 5 and "level 2" in str(ei.value)
 
 
+@pytest.mark.parametrize("name,levels", [("C1", [0, 1, 2]), ("grid5", [0, 1, 2, 3, 4]),
+                                         ("halton3d", [0, 1])])
+@pytest.mark.parametrize("schedule", ["pruned", "literal"])
+def test_kappa_estimate(msk, ctx, name, levels, schedule):
+    """kappa(A_l) estimated from the CG coefficients (Lanczos
+    tridiagonal) of the solve that produced alpha_l, against the dense
+    spectrum lambda_max / lambda_min of A_l (oracle.dense).  Ritz values lie
+    inside [lambda_min, lambda_max], so the estimate is a lower bound; with a
+    smooth right-hand side the extreme eigenvectors are weakly excited, so it
+    is within 10 %, not exact."""
+    from oracle import dense
+    H = HIERS[name]()
+    h = _hier(msk, ctx, H)
+    _, info = h.solve(H.f(), tol=TOL, schedule=schedule)
+    for l in levels:
+        ev = np.linalg.eigvalsh(dense.kernel_matrix(H.points[l], H.points[l], H.delta[l], k=H.k))
+        kap = ev[-1] / ev[0]
+        assert info.cg_iters[l] > 0
+        assert 0.9 * kap <= info.kappa_est[l] <= kap * (1 + 1e-9), (l, info.kappa_est[l], kap)
+
+
 # -------------------------------------------------------------- full solve
 @pytest.mark.parametrize("name", list(HIERS))
 @pytest.mark.parametrize("schedule", ["pruned", "literal"])

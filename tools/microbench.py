@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--level", type=int, default=-1, help="level of the CG / SpMV timings (default finest)")
     ap.add_argument("--eval", action="store_true",
                     help="only time s_L at 1e7 uniform points (first k_gather launch = evaluation)")
     args = ap.parse_args()
@@ -44,7 +45,7 @@ def main():
         print(json.dumps({"config": args.config, "m": 10_000_000, "eval_kernel_ms": ts[1:]}))
         return
     L = H.L
-    lf = L - 1
+    lf = L - 1 if args.level < 0 else args.level
     n, nnz = H.n[lf], int(info.nnz_A[lf])
     out = {"config": args.config, "n": n, "nnz": nnz}
     v = torch.rand(n, dtype=torch.float64, device=dev)
@@ -68,7 +69,7 @@ def main():
     it = its[-1]
     cgb = it * (12.0 * nnz + 88.0 * n) + 16.0 * n   # DESIGN.md §7 (k_cg algorithmic bytes)
     out.update(cg_ms=t, cg_iters=it, cg_ms_per_iter=t / max(it, 1), cg_GBs=cgb / (t * 1e-3) / 1e9)
-    if L > 1:
+    if lf > 0:
         vc = torch.rand(H.n[lf - 1], dtype=torch.float64, device=dev)
         ts = []
         for _ in range(3):
