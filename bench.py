@@ -127,8 +127,10 @@ def run_msk(args, rank, world, local_rank):
     sched = args.schedule
     thr = args.threshold if args.threshold is not None else (3.0 if args.config == "C4" else 0.0)
 
+    hflags = msk.MSK_FLAG_MATRIX_FREE if args.matrix_free else 0
+
     def step(pts, f, xe, alpha, s):
-        h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=H.k)
+        h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=H.k, flags=hflags)
         h.assemble(T=thr, lagrange_tol=1e-14)
         _, sinfo = h.solve(f, tol=args.tol, max_iter=20000, schedule=sched, alpha=alpha)
         _, einfo = h.evaluate(xe, out=s)
@@ -137,7 +139,9 @@ def run_msk(args, rank, world, local_rank):
         return hinfo, sinfo, einfo
 
     def nnz_of(hinfo, sinfo, einfo):
-        return float(sum(hinfo.nnz_A[l] for l in range(L))) + sinfo.nnz_cg + sinfo.nnz_gather + einfo.nnz
+        # assembly evaluates every entry of A once (not in matrix-free mode)
+        assembled = 0.0 if args.matrix_free else float(sum(hinfo.nnz_A[l] for l in range(L)))
+        return assembled + sinfo.nnz_cg + sinfo.nnz_gather + einfo.nnz
 
     def launches_of(hinfo, sinfo, einfo):
         return hinfo.launches_create + hinfo.launches_assemble + sinfo.launches + einfo.launches
@@ -203,7 +207,7 @@ def run_msk(args, rank, world, local_rank):
         # the same iterations; per-rank counters see only owned rows)
         if rank == 0:
             c1 = msk.Context(local_rank, stream.cuda_stream)
-            h1 = msk.Hierarchy(c1, pts_d, H.delta, H.q, k=H.k)
+            h1 = msk.Hierarchy(c1, pts_d, H.delta, H.q, k=H.k, flags=hflags)
             h1.assemble(T=thr, lagrange_tol=1e-14)
             _, si1 = h1.solve(f_d, tol=args.tol, max_iter=20000, schedule=sched)
             _, ei1 = h1.evaluate(xe_d)
@@ -231,6 +235,27 @@ def run_msk(args, rank, world, local_rank):
         with open(tp) as fh:
             traffic = json.load(fh).get("cg_finest_level_bytes_per_launch")
     share = cg_ms / ms if ms > 0 else None
+    if args.matrix_free:
+        # FP64-ALU bound: algorithmic flops = 17 per Wendland nonzero (r^2 5, scale 1,
+        # phi 5 + 1 FMA, accumulate 2, sqrt counted as 3); candidate
+        # tests not counted.  Peak: measured DFMA rate (profiles/fp64_peak.json).
+        fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+        fpeak = json.load(open(fp))["fp64_fma_tflops"] if os.path.exists(fp) else 37.2
+        nnz_f = float(np.mean([r[1].cg_iters[lf] for r in recs])) * float(hinfo.nnz_A[lf])
+        ach = 17.0 * nnz_f / (cg_ms * 1e-3) / 1e12 if cg_ms > 0 else 0.0
+        roof = {"bound": "alu", "achieved": ach, "peak": fpeak, "unit": "TFLOP/s", "frac": ach / fpeak,
+                "traffic": None,
+                "kernel": "k_mf_spmv + CG phase kernels (matrix-free finest level, per-launch average over the solve)",
+                "peak_source": "profiles/fp64_peak.json (measured DFMA)" if os.path.exists(fp) else
+                "derived 148 SM x 64 FP64 lanes x 2 x 1.965 GHz",
+                "algorithmic_flops_per_solve": 17.0 * nnz_f, "launch_ms": cg_ms, "share_of_step": share}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_cg (persistent cooperative CG, finest level: fused CSR SpMV + dots + updates)",
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "algorithmic_bytes_per_launch": cg_bytes, "launch_ms": cg_ms,
+                "share_of_step": share}
 
     out = {
         "metric": METRIC, "value": nnz_all / (ms * 1e-3) / 1e9, "unit": UNIT,
@@ -240,6 +265,7 @@ def run_msk(args, rank, world, local_rank):
         "data": "synthetic",
         "config": {"workload": WORKLOAD if args.config == "C3" else args.config,
                    "config": args.config, "schedule": sched, "tol": args.tol, "threshold_T": thr,
+                   "matrix_free": bool(args.matrix_free),
                    "n_per_level": H.n, "nnz_A": [int(hinfo.nnz_A[l]) for l in range(L)],
                    "cg_iters": [int(sinfo.cg_iters[l]) for l in range(L)],
                    "kappa_est": [round(float(sinfo.kappa_est[l]), 2) for l in range(L)],
@@ -254,12 +280,7 @@ def run_msk(args, rank, world, local_rank):
                                 "solve_cg_per_level": [sinfo.t_cg_level_ms[l] for l in range(L)],
                                 "solve_b_products": sinfo.t_gather_ms, "evaluate": einfo.t_total_ms,
                                 "evaluate_sort": einfo.t_sort_ms, "evaluate_kernel": einfo.t_eval_ms}},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_cg (persistent cooperative CG, finest level: fused CSR SpMV + dots + updates)",
-                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "algorithmic_bytes_per_launch": cg_bytes, "launch_ms": cg_ms,
-                     "share_of_step": share},
+        "roofline": roof,
         "e2e": {"value": e2e_nnz_all / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
@@ -349,6 +370,8 @@ def main():
     ap.add_argument("--threshold", type=float, default=None,
                     help="T of the thresholded factor (C4 default 3; 0 = exact mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--matrix-free", action="store_true",
+                    help="MSK_FLAG_MATRIX_FREE: A_l never stored, CG SpMVs evaluate Phi on the fly")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))

@@ -71,6 +71,12 @@ typedef enum {
 #define MSK_FLAG_DIST_ALL 1u /* distributed context: partition every level that has at least world
                                 row chunks (default: only levels with >= 2^20 points; smaller
                                 levels are solved redundantly on every rank) */
+#define MSK_FLAG_MATRIX_FREE 2u /* a3 matrix-free: A_l is never stored;
+                                   every CG SpMV evaluates Phi on the fly over the level's cell list,
+                                   visiting the columns in the stored CSR order, so alpha is
+                                   BIT-IDENTICAL to the assembled solve.  msk_assemble(T > 0),
+                                   the LITERAL schedule and msk_cg_level are MSK_ERR_INVALID /
+                                   MSK_ERR_STATE on such a hierarchy (PRUNED only) */
 
 /* msk_solve schedules */
 #define MSK_SCHED_PRUNED 0u  /* Algorithm 2 with each inner solve t^{(l)} = A_l^{-1} beta^{(l)} done

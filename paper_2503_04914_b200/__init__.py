@@ -16,7 +16,7 @@ import weakref
 import numpy as np
 
 from . import _lib
-from ._lib import (EXPORTED, MSK_FLAG_DIST_ALL, MSK_SCHED_LITERAL, MSK_SCHED_PRUNED, EvalInfo, HierarchyInfo,
+from ._lib import (EXPORTED, MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE, MSK_SCHED_LITERAL, MSK_SCHED_PRUNED, EvalInfo, HierarchyInfo,
                    MskError, SolveInfo, check, load)
 
 __all__ = ["Context", "Hierarchy", "MskError", "SolveInfo", "HierarchyInfo", "EvalInfo",

@@ -105,6 +105,7 @@ EXPORTED = ["msk_ctx_create", "msk_ctx_destroy", "msk_hierarchy_create", "msk_hi
             "msk_export_block", "msk_export_factor", "msk_export_cells", "msk_apply_block", "msk_cg_level",
             "msk_nccl_unique_id", "msk_partition_rows", "msk_halo_plan", "msk_last_error", "msk_version"]
 MSK_FLAG_DIST_ALL = 1
+MSK_FLAG_MATRIX_FREE = 2
 
 
 def check(status: int) -> None:

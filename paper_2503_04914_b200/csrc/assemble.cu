@@ -73,7 +73,50 @@ __global__ void __launch_bounds__(NT) k_fill(LevelView rows, LevelView cols,
         }
     });
 }
+template <int D>
+__global__ void __launch_bounds__(NT) k_hit_range(LevelView rows, LevelView cols,
+                                                  unsigned long long *__restrict__ mm) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    unsigned long long lo = ~0ull, hi = 0;
+    if (i < rows.n) {
+        double x[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = rows.x[a][i];
+        const double d2 = cols.delta2;
+        for_each_range<D>(cols, x, [&](int b, int e) {
+            for (int j = b; j < e; ++j) {
+                double y[3];
+#pragma unroll
+                for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
+                if (dist2_nofma<D>(x, y) < d2) {
+                    lo = (unsigned long long)j < lo ? (unsigned long long)j : lo;
+                    hi = (unsigned long long)j > hi ? (unsigned long long)j : hi;
+                }
+            }
+        });
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, lo, o);
+        lo = t < lo ? t : lo;
+        t = __shfl_xor_sync(0xffffffffu, hi, o);
+        hi = t > hi ? t : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
 }  // namespace
+
+void hit_range(int d, const LevelView &rows, const LevelView &cols, unsigned long long *mm, cudaStream_t st) {
+    unsigned long long init[2] = {~0ull, 0ull};
+    MSK_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+    if (rows.n == 0) return;
+    unsigned nb = ceil_div_u(rows.n, NT);
+    if (d == 2) k_hit_range<2><<<nb, NT, 0, st>>>(rows, cols, mm);
+    else k_hit_range<3><<<nb, NT, 0, st>>>(rows, cols, mm);
+    MSK_CHECK_LAUNCH();
+}
 
 void count_pattern(int d, const LevelView &rows, const LevelView &cols, bool same, int32_t *cnt,
                    unsigned long long *min_r2_bits, cudaStream_t st, int *launches) {

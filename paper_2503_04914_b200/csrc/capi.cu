@@ -396,7 +396,7 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
         require(d == 2 || d == 3, "msk_hierarchy_create: d must be 2 or 3");
         require(L >= 1 && L <= kMaxLevels, "msk_hierarchy_create: L must be in 1..16");
         require(wendland_k >= 0 && wendland_k <= 2, "msk_hierarchy_create: k must be 0, 1 or 2");
-        require((flags & ~MSK_FLAG_DIST_ALL) == 0, "msk_hierarchy_create: unknown flags");
+        require((flags & ~(MSK_FLAG_DIST_ALL | MSK_FLAG_MATRIX_FREE)) == 0, "msk_hierarchy_create: unknown flags");
         for (int l = 0; l < L; ++l) {
             require(n[l] >= 1 && n[l] < (1ll << 31) - 1, "msk_hierarchy_create: n[l] out of range");
             require(points[l] != nullptr, "msk_hierarchy_create: NULL points");
@@ -668,6 +668,9 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
     require(!(T > 0.0) || (lagrange_tol > 0.0 && lagrange_tol < 1.0),
             "msk_assemble: lagrange_tol must be in (0,1) when T > 0");
     require(!(T > 0.0) || h->ctx->world == 1, "msk_assemble: the thresholded factor is single-GPU in this version");
+    require(!(T > 0.0) || !(h->flags & MSK_FLAG_MATRIX_FREE),
+            "msk_assemble: the thresholded factor needs assembled A_l (hierarchy is MSK_FLAG_MATRIX_FREE)");
+    const bool mf = (h->flags & MSK_FLAG_MATRIX_FREE) != 0;
     MSK_CUDA(cudaSetDevice(h->ctx->device));
     cudaStream_t st = h->st();
     h->release_factor();
@@ -726,6 +729,21 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
             auto &Dd = h->dist[l];
             unsigned long long *mm = dalloc<unsigned long long>(2, st);
             for (auto &P : Dd.local) {
+                if (mf) {  // no stored entries: nnz from the row counts, halo from the hit range
+                    dfree(P.rp, st);
+                    P.rp = nullptr;
+                    LevelView rows = h->view(l), cols = h->view(l);
+                    rows.n = P.hi - P.lo;
+                    for (int a = 0; a < h->d; ++a) rows.x[a] += P.lo;
+                    hit_range(h->d, rows, cols, mm, st);
+                    unsigned long long hm[2];
+                    MSK_CUDA(cudaMemcpyAsync(hm, mm, sizeof hm, cudaMemcpyDeviceToHost, st));
+                    MSK_CUDA(cudaStreamSynchronize(st));
+                    P.hlo = P.nnz ? std::min<int64_t>((int64_t)hm[0], P.lo) : P.lo;
+                    P.hhi = P.nnz ? std::max<int64_t>((int64_t)hm[1] + 1, P.hi) : P.hi;
+                    D.nnz += P.nnz;
+                    continue;
+                }
                 P.col = dalloc<int32_t>((size_t)P.nnz + 4, st);
                 P.val = dalloc<double>((size_t)P.nnz + 2, st);
                 MSK_CUDA(cudaMemsetAsync(P.col + P.nnz, 0, 4 * sizeof(int32_t), st));
@@ -762,6 +780,11 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
             continue;
         }
         D.nnz = nnz[l];
+        if (mf) {  // matrix-free: the row counts (nnz) are all that is kept
+            dfree(D.row_ptr, st);
+            D.row_ptr = nullptr;
+            continue;
+        }
         D.col = dalloc<int32_t>((size_t)D.nnz + 4, st);  // + padding for 16-byte bulk copies
         D.val = dalloc<double>((size_t)D.nnz + 2, st);
         MSK_CUDA(cudaMemsetAsync(D.col + D.nnz, 0, 4 * sizeof(int32_t), st));
@@ -880,6 +903,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     cudaStream_t st = h->st();
     const int L = h->L;
     const double inner_tol = tol / 10.0;  // reading C-10
+    const bool mf = (h->flags & MSK_FLAG_MATRIX_FREE) != 0;
     h->ensure_ws();
     for (int l = 0; l < L; ++l)
         if (!h->lev[l].alpha) h->lev[l].alpha = dalloc<double>((size_t)h->lev[l].n, st);
@@ -958,8 +982,18 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         const int64_t n = D.n;
         const int CH = cg_chunk_tiles(n);
         const int64_t nch = (n + (int64_t)CH * 256 - 1) / ((int64_t)CH * 256);
-        const int np = (int)Dd.local.size();
-        const bool emu = h->ctx->emulated;
+        // a partitioned level, or (matrix-free, not partitioned) one partition of all rows
+        const bool part = Dd.on;
+        std::vector<msk_hierarchy::PartLocal> whole;
+        if (!part) {
+            msk_hierarchy::PartLocal P;
+            P.lo = 0; P.hi = n; P.c0 = 0; P.c1 = nch; P.nnz = D.nnz; P.hlo = 0; P.hhi = n;
+            whole.push_back(P);
+        }
+        auto &parts = part ? Dd.local : whole;
+        const int np = (int)parts.size();
+        const bool emu = part && h->ctx->emulated;
+        const int W = part ? h->ctx->world : 1;
         std::vector<double *> X(np), R(np), Pv(np), Q(np), send(np);
         std::vector<double *> owned_alloc;
         double *recv = dalloc<double>((size_t)nch, st);
@@ -977,7 +1011,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         }
         // beta^(l) on the owned rows (B products of the coarser, complete levels)
         if (l > 0) {
-            for (auto &P : Dd.local) {
+            for (auto &P : parts) {
                 GatherArgs ga{};
                 ga.d = h->d;
                 ga.k = h->k;
@@ -997,14 +1031,14 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         }
         std::vector<DistCGArgs> args(np);
         for (int i = 0; i < np; ++i) {
-            const auto &P = Dd.local[i];
+            const auto &P = parts[i];
             DistCGArgs &A = args[i];
             A.L = cg_args(h, l, tl, max_iter, l == 0 ? nullptr : h->ws_beta(l), l == 0 ? fd[0].ptr : nullptr,
                           X[i], nullptr, nullptr, nullptr, nullptr);
             A.L.r = R[i];
             A.L.p = Pv[i];
             A.L.q = Q[i];
-            A.L.row_ptr = P.rp - P.lo;  // indexed by global row
+            A.L.row_ptr = P.rp ? P.rp - P.lo : nullptr;  // indexed by global row
             A.L.col = P.col;
             A.L.val = P.val;
             A.L.nnz = P.nnz;
@@ -1013,11 +1047,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             A.c1 = P.c1;
             A.nchunks = nch;
             A.part_send = send[i];
-            A.part_recv = recv;
+            A.part_recv = part ? recv : send[i];  // one partition: nothing to reduce
             A.sc = sc + i;
             if (i == 0) set_coef(A.L, l);
         }
         auto allreduce = [&]() {
+            if (!part) return;
             if (emu) {
                 DistPtrs ptrs{};
                 for (int i = 0; i < np; ++i) ptrs.p[i] = send[i];
@@ -1027,12 +1062,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             }
         };
         // halo plans (msk_halo_plan): per local partition, send/recv row ranges per peer
-        const int W = h->ctx->world;
         std::vector<std::vector<int64_t>> sl(np, std::vector<int64_t>(W)), sh = sl, rl = sl, rh = sl;
-        for (int i = 0; i < np; ++i)
-            msk_halo_plan(W, Dd.local[i].rank, Dd.rows.data(), Dd.hlo.data(), Dd.hhi.data(), sl[i].data(),
+        for (int i = 0; i < np && part; ++i)
+            msk_halo_plan(W, parts[i].rank, Dd.rows.data(), Dd.hlo.data(), Dd.hhi.data(), sl[i].data(),
                           sh[i].data(), rl[i].data(), rh[i].data());
         auto halo = [&]() {
+            if (!part) return;
             if (emu) {  // partition i receives from partition s by a device copy
                 for (int i = 0; i < np; ++i)
                     for (int s = 0; s < W; ++s)
@@ -1061,7 +1096,10 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         launches += 3 * np;
         for (int done = 0;;) {
             for (int k = 0; k < 8; ++k) {
-                for (int i = 0; i < np; ++i) dcg_spmv(args[i], st);
+                for (int i = 0; i < np; ++i) {
+                    if (mf) dcg_mf_spmv(args[i], h->view(l), h->d, h->k, st);
+                    else dcg_spmv(args[i], st);
+                }
                 allreduce();
                 for (int i = 0; i < np; ++i) dcg_scalar(args[i], 1, st);
                 for (int i = 0; i < np; ++i) dcg_rupd(args[i], st);
@@ -1081,9 +1119,11 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         launches += np;
         cg_t.back()->stop();
         // alpha^(l) complete on every rank (spatial order), then caller order
-        if (emu) {
+        if (!part) {
+            MSK_CUDA(cudaMemcpyAsync(alpha_sp[l], X[0], sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        } else if (emu) {
             for (int i = 0; i < np; ++i) {
-                const auto &P = Dd.local[i];
+                const auto &P = parts[i];
                 MSK_CUDA(cudaMemcpyAsync(alpha_sp[l] + P.lo, X[i] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
                                          cudaMemcpyDeviceToDevice, st));
             }
@@ -1108,6 +1148,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     bool any_dist = false;
     for (int l = 0; l < L; ++l) any_dist = any_dist || h->dist[l].on;
     require(!any_dist || schedule == MSK_SCHED_PRUNED, "msk_solve: a distributed solve uses the PRUNED schedule");
+    require(!mf || schedule == MSK_SCHED_PRUNED, "msk_solve: a matrix-free hierarchy uses the PRUNED schedule");
 
     const bool thresholded = h->T > 0.0;
     if (thresholded) {
@@ -1155,7 +1196,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         // same solve); the finest level is solved at tol.
         for (int l = 0; l < L; ++l) {
             const double tl = l + 1 < L ? inner_tol : tol;
-            if (h->dist[l].on) {
+            if (h->dist[l].on || mf) {
                 dist_level(l, tl);
                 debug_sync(st, "dist_level");
                 if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);
@@ -1374,7 +1415,7 @@ extern "C" msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_
     double *vl = nullptr;
     bool own = true;
     int64_t nnz = 0;
-    if (row_level == col_level && h->assembled && !h->dist[row_level].on) {
+    if (row_level == col_level && h->assembled && !h->dist[row_level].on && R.row_ptr) {
         rp = R.row_ptr; cl = R.col; vl = R.val; nnz = R.nnz;
         own = false;
     } else {
@@ -1509,7 +1550,7 @@ extern "C" msk_status msk_apply_block(msk_hierarchy *h, int row_level, int col_l
     double *vs = dalloc<double>((size_t)C.n, st);
     permute_gather(C.n, vd.ptr, C.perm, vs, st, nullptr);
     Timer tm(st);
-    if (row_level == col_level) {
+    if (row_level == col_level && R.row_ptr) {
         double *ys = dalloc<double>((size_t)R.n, st);
         tm.start();
         spmv_csr(R.n, R.row_ptr, R.col, R.val, vs, ys, st, nullptr);
@@ -1547,6 +1588,8 @@ extern "C" msk_status msk_cg_level(msk_hierarchy *h, int level, const double *b,
     require(tol > 0.0 && tol < 1.0 && max_iter >= 1, "msk_cg_level: bad tol / max_iter");
     if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_cg_level: assemble first");
     if (h->dist[level].on) throw Error(MSK_ERR_STATE, "msk_cg_level: level is partitioned across ranks");
+    if (h->flags & MSK_FLAG_MATRIX_FREE)
+        throw Error(MSK_ERR_STATE, "msk_cg_level: matrix-free hierarchy (no stored A_l); use msk_solve");
     MSK_CUDA(cudaSetDevice(h->ctx->device));
     cudaStream_t st = h->st();
     h->ensure_ws();

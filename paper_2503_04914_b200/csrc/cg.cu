@@ -44,6 +44,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "neighbors.cuh"
 #include "tma.cuh"
 
 namespace msk {
@@ -53,7 +54,16 @@ constexpr int NT = 256;       // threads per CTA == rows per tile
 constexpr int NW = NT / 32;   // warps per CTA
 constexpr int CAPW = 224;     // CSR entries per warp pipeline stage (values 1.75 KB + columns 0.9 KB)
 constexpr int CAPWE = CAPW - 2;  // usable entries per stage (16-byte alignment slack)
-constexpr int U = 4;          // independent gathers in flight per lane (row-parallel)
+#ifndef MSK_U
+#define MSK_U 4
+#endif
+#ifndef MSK_CAPT
+#define MSK_CAPT 2048
+#endif
+#ifndef MSK_MINB
+#define MSK_MINB 3
+#endif
+constexpr int U = MSK_U;      // independent gathers in flight per lane (row-parallel)
 constexpr int MAXCH = 4;      // max tiles per chunk
 constexpr int RPCAP = MAXCH * NT + 4;  // staged row pointers per chunk
 
@@ -76,7 +86,7 @@ struct __align__(16) CGShared {
 };
 
 // ---- CTA-level pipeline (used by k_cg): large bulk copies, double-buffered
-constexpr int CAPT = 2048;        // CSR entries per stage (values 16 KB + columns 8 KB)
+constexpr int CAPT = MSK_CAPT;    // CSR entries per stage (2048: values 16 KB + columns 8 KB)
 constexpr int CAPTE = CAPT - 2;   // usable entries per piece (alignment slack)
 constexpr int NSTG = 2;           // pipeline stages (NSTG - 1 pieces in flight ahead)
 struct __align__(16) CtaStage {
@@ -442,7 +452,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
     ps.CS += (uint32_t)K;
 }
 
-__global__ void __launch_bounds__(NT, 3) k_cg(CGBatch B) {
+__global__ void __launch_bounds__(NT, MSK_MINB) k_cg(CGBatch B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CGSharedT &S = *reinterpret_cast<CGSharedT *>(smem_raw);
 
@@ -620,7 +630,7 @@ __global__ void __launch_bounds__(NT) k_dcg_init(DistCGArgs A) {
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) k_dcg_spmv(DistCGArgs A) {
+__global__ void __launch_bounds__(NT, MSK_MINB) k_dcg_spmv(DistCGArgs A) {
     if (!A.sc->active) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CGSharedT &S = *reinterpret_cast<CGSharedT *>(smem_raw);
@@ -670,6 +680,81 @@ __global__ void __launch_bounds__(NT) k_dcg_xfin(DistCGArgs A) {
             int64_t i = (c * CH + t) * NT + tid;
             if (i < L.n) L.x[i] = any ? L.x[i] + alpha * L.p[i] : 0.0;
         }
+}
+
+// Matrix-free pass 1 (MSK_FLAG_MATRIX_FREE): per owned row i, w = sum_j
+// Phi(x_i - x_j) r_j with Phi evaluated exactly as k_fill stores it
+// (scale * phi(sqrt(r2) / delta)) and the hits visited in ascending j -- the
+// CSR column order -- so w, and with the same epilogue and chunk partials as
+// spmv_phase the whole CG, is bit-identical to the assembled path.
+// Candidates: conservative FP32 prefilter (gather.cu), then the exact no-FMA
+// test (reading C-4) on the survivors.
+template <int D, int K>
+__global__ void __launch_bounds__(NT, 3) k_mf_spmv(DistCGArgs A, LevelView V) {
+    if (!A.sc->active) return;
+    __shared__ double red[NT / 32 + 2];
+    constexpr int HM = 40;
+    const CGLevelArgs &L = A.L;
+    const int CH = L.chunk_tiles, tid = threadIdx.x;
+    const bool first = A.sc->it == 0;
+    const double alpha_prev = A.sc->alpha, beta = A.sc->beta;
+    const double *rv = L.r;
+    const double d2 = V.delta2, inv = V.inv_delta, scl = V.scale;
+    const float fthr = V.fthr;
+    const float4 *__restrict__ frec = V.frec;
+    for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x) {
+        double dot = 0.0;
+        for (int t = 0; t < CH; ++t) {
+            const int64_t i = (c * CH + t) * NT + tid;
+            if (i >= L.n) continue;
+            double x[3];
+            float xf[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                x[a] = V.x[a][i];
+                xf[a] = (float)(x[a] - V.g.lo[a]);
+            }
+            double acc = 0.0;
+            int hl[HM];
+            int nh = 0;
+            auto flush = [&]() {
+                for (int h = 0; h < nh; ++h) {
+                    const int j = hl[h];
+                    double y[3];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) y[a] = V.x[a][j];
+                    const double r2 = dist2_nofma<D>(x, y);
+                    if (r2 < d2) {
+                        const double v = scl * wendland<K>(sqrt(r2) * inv);
+                        acc = fma(v, rv[j], acc);
+                    }
+                }
+                nh = 0;
+            };
+            for_each_range<D>(V, x, [&](int b, int e) {
+                for (int j = b; j < e; ++j) {
+                    const float4 F = frec[j];
+                    const float a0 = xf[0] - F.x, b0 = xf[1] - F.y, c0 = xf[2] - F.z;
+                    if (fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr) {
+                        if (nh == HM) flush();
+                        hl[nh++] = j;
+                    }
+                }
+            });
+            flush();
+            // epilogue: the expressions of spmv_phase
+            const double ri = rv[i];
+            const double po = first ? 0.0 : L.p[i], qo = first ? 0.0 : L.q[i], xo = first ? 0.0 : L.x[i];
+            const double pn = first ? ri : ri + beta * po;
+            const double qn = first ? acc : acc + beta * qo;
+            L.p[i] = pn;
+            L.q[i] = qn;
+            L.x[i] = first ? 0.0 : xo + alpha_prev * po;
+            dot += pn * qn;
+        }
+        const double s = block_sum<NT>(dot, red);
+        if (tid == 0) A.part_send[c] = s;
+    }
 }
 
 // mode 0: after init (bb); 1: after SpMV (pq, alpha); 2: after the r update
@@ -859,6 +944,16 @@ void dcg_rupd(const DistCGArgs &a, cudaStream_t st) {
 }
 void dcg_xfin(const DistCGArgs &a, cudaStream_t st) {
     k_dcg_xfin<<<dcg_grid(a, 8), NT, 0, st>>>(a);
+    MSK_CHECK_LAUNCH();
+}
+void dcg_mf_spmv(const DistCGArgs &a, const LevelView &v, int d, int k, cudaStream_t st) {
+#define MSK_MF(DD, KK) k_mf_spmv<DD, KK><<<dcg_grid(a, 3), NT, 0, st>>>(a, v)
+    if (d == 2) {
+        if (k == 0) MSK_MF(2, 0); else if (k == 1) MSK_MF(2, 1); else MSK_MF(2, 2);
+    } else {
+        if (k == 0) MSK_MF(3, 0); else if (k == 1) MSK_MF(3, 1); else MSK_MF(3, 2);
+    }
+#undef MSK_MF
     MSK_CHECK_LAUNCH();
 }
 void dcg_scalar(const DistCGArgs &a, int mode, cudaStream_t st) {
