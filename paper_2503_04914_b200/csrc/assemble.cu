@@ -1,7 +1,8 @@
 // assemble.cu -- a2: CSR pattern and values of A_l (and of B_{kl} blocks for
 // export).  Pattern: r^2 < delta^2 with r^2 evaluated left to right without
 // FMA and delta^2 computed once on the host (reading C-4) -- bit-exact with
-// the definition.  Values Phi_delta(r) = delta^-d phi(r / delta)
+// the definition; candidates are screened by the conservative FP32 prefilter
+// first (for_each_hit, neighbors.cuh), which never drops a true neighbour.  Values Phi_delta(r) = delta^-d phi(r / delta)
 // (eq:kernelscaling P:67) with the column level's delta (reading C-1).
 #include "kernels.cuh"
 #include "neighbors.cuh"
@@ -22,18 +23,9 @@ __global__ void __launch_bounds__(NT) k_count(LevelView rows, LevelView cols, in
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = rows.x[a][i];
         int c = 0;
-        const double d2 = cols.delta2;
-        for_each_range<D>(cols, x, [&](int b, int e) {
-            for (int j = b; j < e; ++j) {
-                double y[3];
-#pragma unroll
-                for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
-                double r2 = dist2_nofma<D>(x, y);
-                if (r2 < d2) {
-                    ++c;
-                    if (same && j != i && r2 < best) best = r2;
-                }
-            }
+        for_each_hit<D>(cols, x, [&](int j, double r2) {
+            ++c;
+            if (same && j != i && r2 < best) best = r2;
         });
         cnt[i] = c;
     }
@@ -58,19 +50,11 @@ __global__ void __launch_bounds__(NT) k_fill(LevelView rows, LevelView cols,
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = rows.x[a][i];
     int64_t p = row_ptr[i];
-    const double d2 = cols.delta2, inv = cols.inv_delta, sc = cols.scale;
-    for_each_range<D>(cols, x, [&](int b, int e) {
-        for (int j = b; j < e; ++j) {
-            double y[3];
-#pragma unroll
-            for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
-            double r2 = dist2_nofma<D>(x, y);
-            if (r2 < d2) {
-                col[p] = j;
-                if (val) val[p] = sc * wendland<K>(sqrt(r2) * inv);
-                ++p;
-            }
-        }
+    const double inv = cols.inv_delta, sc = cols.scale;
+    for_each_hit<D>(cols, x, [&](int j, double r2) {
+        col[p] = j;
+        if (val) val[p] = sc * wendland<K>(sqrt(r2) * inv);
+        ++p;
     });
 }
 template <int D>
@@ -82,17 +66,9 @@ __global__ void __launch_bounds__(NT) k_hit_range(LevelView rows, LevelView cols
         double x[3];
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = rows.x[a][i];
-        const double d2 = cols.delta2;
-        for_each_range<D>(cols, x, [&](int b, int e) {
-            for (int j = b; j < e; ++j) {
-                double y[3];
-#pragma unroll
-                for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
-                if (dist2_nofma<D>(x, y) < d2) {
-                    lo = (unsigned long long)j < lo ? (unsigned long long)j : lo;
-                    hi = (unsigned long long)j > hi ? (unsigned long long)j : hi;
-                }
-            }
+        for_each_hit<D>(cols, x, [&](int j, double) {
+            lo = (unsigned long long)j < lo ? (unsigned long long)j : lo;
+            hi = (unsigned long long)j > hi ? (unsigned long long)j : hi;
         });
     }
     for (int o = 16; o > 0; o >>= 1) {

@@ -1088,6 +1088,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 MSK_NCCL(nccl_api()->GroupEnd());
             }
         };
+        if (mf) h->pack(l, h->ws_r(l), &launches);  // packed coordinates for k_mf_spmv
         time_cg(l);
         for (int i = 0; i < np; ++i) dcg_init(args[i], st);
         allreduce();

@@ -85,20 +85,31 @@ struct __align__(16) CGShared {
     uint64_t wbar[NW][2];     // per-warp, per-stage barriers
 };
 
-// ---- CTA-level pipeline (used by k_cg): large bulk copies, double-buffered
-constexpr int CAPT = MSK_CAPT;    // CSR entries per stage (2048: values 16 KB + columns 8 KB)
-constexpr int CAPTE = CAPT - 2;   // usable entries per piece (alignment slack)
+// ---- CTA-level pipeline (used by k_cg): large bulk copies, double-buffered.
+// The piece capacity C (CSR entries per stage) is a template parameter: the
+// launcher picks C from the mean row length so that a piece spans ~200+ rows
+// (each thread owns rows, so a piece of few long rows leaves threads idle):
+// C = 2048 (values 16 KB + columns 8 KB, 3 CTAs/SM) for short rows (d = 3),
+// C = 4096 (2 CTAs/SM) for long rows (d = 2, ~25 per row).  Same-box A/B:
+// C3 finest level 33.5 ms (2048) vs 37.7 (4096); C5 finest 1546 vs 1246 ms.
+constexpr int CAPT0 = MSK_CAPT;   // short-row variant
+constexpr int MINB0 = MSK_MINB;
+constexpr int CAPT1 = 4096;       // long-row variant
+constexpr int MINB1 = 2;
 constexpr int NSTG = 2;           // pipeline stages (NSTG - 1 pieces in flight ahead)
-struct __align__(16) CtaStage {
-    double val[CAPT];
-    int32_t col[CAPT + 8];
+template <int C>
+struct __align__(16) CtaStageT {
+    double val[C];
+    int32_t col[C + 8];
 };
-struct __align__(16) CGSharedT {
-    CtaStage st[NSTG];        // ring of CSR slices (a stream of pieces)
+template <int C>
+struct __align__(16) CGSharedTT {
+    CtaStageT<C> st[NSTG];    // ring of CSR slices (a stream of pieces)
     int64_t rp[2][RPCAP];     // row pointers of the current and the next chunk
     double red[NT / 32 + 2];
     uint64_t bar_st[NSTG];
     uint64_t bar_rp[2];
+    uint64_t bar_empty[NSTG];  // MSK_EMPTYBAR: one arrival per warp when a stage is consumed
 };
 
 __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
@@ -108,14 +119,14 @@ __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
         round += (unsigned long long)nb;
         if (threadIdx.x == 0) {
             cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*ctr);
-            __threadfence();
+            // release: this CTA's writes (ordered before by __syncthreads) become
+            // visible to every CTA that acquires the counter (no extra fence)
             a.fetch_add(1ull, cuda::memory_order_release);
             unsigned long long spins = 0;
             while (a.load(cuda::memory_order_acquire) < round) {
                 __nanosleep(32);
                 if (++spins > (1ull << 31)) __trap();  // never hang the device forever
             }
-            __threadfence();
         }
         __syncthreads();
     }
@@ -295,7 +306,8 @@ struct PipeState {
     uint32_t CS;  // chunks visited so far (rp buffer CS&1, parity (CS>>1)&1)
 };
 
-__device__ __forceinline__ void issue_rp(CGSharedT &S, int b, const int64_t *row_ptr, int64_t r0, int nrows,
+template <class SH>
+__device__ __forceinline__ void issue_rp(SH &S, int b, const int64_t *row_ptr, int64_t r0, int nrows,
                                          uint64_t pol) {
     const int64_t lo = r0 & ~(int64_t)1;
     const int64_t hi = (r0 + nrows + 2) & ~(int64_t)1;
@@ -304,7 +316,16 @@ __device__ __forceinline__ void issue_rp(CGSharedT &S, int b, const int64_t *row
     tma_load_1d(S.rp[b], row_ptr + lo, bytes, &S.bar_rp[b], pol);
 }
 
-__device__ __forceinline__ void issue_piece_t(CGSharedT &S, int b, const int32_t *col, const double *val,
+// before issuing piece Q into stage Q % 2: piece Q - 2 (same stage) consumed by every warp
+template <class SH>
+__device__ __forceinline__ void stage_free(SH &S, uint32_t Q) {
+#ifdef MSK_EMPTYBAR
+    if (Q >= 2) mbar_wait(&S.bar_empty[Q & 1], ((Q - 2) >> 1) & 1u);
+#endif
+}
+
+template <class SH>
+__device__ __forceinline__ void issue_piece_t(SH &S, int b, const int32_t *col, const double *val,
                                               int64_t kb, int64_t ke, uint64_t pol) {
     const int64_t vlo = kb & ~(int64_t)1, vhi = (ke + 1) & ~(int64_t)1;
     const int64_t clo = kb & ~(int64_t)3, chi = (ke + 3) & ~(int64_t)3;
@@ -317,9 +338,11 @@ __device__ __forceinline__ void issue_piece_t(CGSharedT &S, int b, const int32_t
 // Chunks handled: cbase + me + k*nb for k = 0.. while < cbase + nloc (cbase =
 // 0, nloc = all chunks on one GPU; the owned chunk range of a partition in
 // the distributed CG).  L.row_ptr is indexed by global row.
-__device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
+template <int C>
+__device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
                                            int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol,
                                            bool first, double alpha_prev, double beta) {
+    constexpr int CAPTE = C - 2;  // usable entries per piece (alignment slack)
     const int tid = threadIdx.x;
     const int64_t n = L.n;
     const int64_t K = me < nloc ? (nloc - 1 - me) / nb + 1 : 0;  // my chunks
@@ -346,11 +369,28 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
     {
         const int64_t *rp = S.rp[ps.CS & 1] + rp_off(cr0);
         const int64_t K0 = rp[0], K1 = rp[crows];
-        if (tid == 0) issue_piece_t(S, ps.P & 1, L.col, L.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
+        if (tid == 0) {
+            stage_free(S, ps.P);
+            issue_piece_t(S, ps.P & 1, L.col, L.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
+        }
     }
     for (int64_t k = 0; k < K; ++k) {
         chunk_rows(k, cr0, crows);
         const uint32_t cs = ps.CS + (uint32_t)k;
+#ifdef MSK_PF
+        // the epilogue's own-row vectors of the NEXT chunk -> L2 (hidden behind this chunk's pieces)
+        if (tid == 0 && !first && k + 1 < K) {
+            int64_t nr0;
+            int nrows;
+            chunk_rows(k + 1, nr0, nrows);
+            // 16-byte aligned interior of each slice (vector bases are only 8-byte aligned)
+            for (const double *v : {(const double *)L.p, (const double *)L.q, (const double *)L.x}) {
+                const uintptr_t a0 = ((uintptr_t)(v + nr0) + 15) & ~(uintptr_t)15;
+                const uintptr_t a1 = (uintptr_t)(v + nr0 + nrows) & ~(uintptr_t)15;
+                if (a1 > a0) prefetch_l2((const void *)a0, (uint32_t)(a1 - a0));
+            }
+        }
+#endif
         const int64_t *rp = S.rp[cs & 1] + rp_off(cr0);
         const int64_t K1 = rp[crows];
         int64_t rb[MAXCH], re[MAXCH];
@@ -368,11 +408,14 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
             // the next piece (rest of this chunk, or the first piece of the next
             // one) goes into the other stage, which held piece P-1 (consumed)
             if (ke < K1) {
-                if (tid == 0)
+                if (tid == 0) {
+                    stage_free(S, ps.P + 1);
                     issue_piece_t(S, (ps.P + 1) & 1, L.col, L.val, ke, ke + CAPTE < K1 ? ke + CAPTE : K1, pol);
+                }
             } else if (k + 1 < K) {
                 mbar_wait(&S.bar_rp[(cs + 1) & 1], ((cs + 1) >> 1) & 1u);
                 if (tid == 0) {
+                    stage_free(S, ps.P + 1);
                     int64_t nr0;
                     int nrows;
                     chunk_rows(k + 1, nr0, nrows);
@@ -382,7 +425,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
                 }
             }
             mbar_wait(&S.bar_st[ps.P & 1], (ps.P >> 1) & 1u);
-            const CtaStage &cur = S.st[ps.P & 1];
+            const CtaStageT<C> &cur = S.st[ps.P & 1];
             const int voff = (int)(kb & 1), coff = (int)(kb & 3);
 #pragma unroll
             for (int t = 0; t < MAXCH; ++t) {
@@ -404,7 +447,12 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
                         if (e + u < hi) acc[t] = fma(vv[u], pv[u], acc[t]);
                 }
             }
+#ifdef MSK_EMPTYBAR
+            __syncwarp();  // this warp is done with stage P%NSTG
+            if ((tid & 31) == 0) mbar_arrive(&S.bar_empty[ps.P & 1]);
+#else
             __syncthreads();  // stage P%NSTG consumed by every thread: it may be refilled
+#endif
             ++ps.P;
             kb = ke;
         }
@@ -452,9 +500,10 @@ __device__ __forceinline__ void spmv_phase(CGSharedT &S, const CGLevelArgs &L, i
     ps.CS += (uint32_t)K;
 }
 
-__global__ void __launch_bounds__(NT, MSK_MINB) k_cg(CGBatch B) {
+template <int C, int MB>
+__global__ void __launch_bounds__(NT, MB) k_cg(CGBatch B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CGSharedT &S = *reinterpret_cast<CGSharedT *>(smem_raw);
+    CGSharedTT<C> &S = *reinterpret_cast<CGSharedTT<C> *>(smem_raw);
 
     int g = 0;
     while (g + 1 < B.nlev && (int)blockIdx.x >= B.lev[g + 1].block_begin) ++g;
@@ -470,6 +519,7 @@ __global__ void __launch_bounds__(NT, MSK_MINB) k_cg(CGBatch B) {
     PipeState ps{0u, 0u};
     if (tid == 0) {
         for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_empty[b], NW);
         mbar_init(&S.bar_rp[0], 1);
         mbar_init(&S.bar_rp[1], 1);
         fence_mbar_init();
@@ -630,12 +680,14 @@ __global__ void __launch_bounds__(NT) k_dcg_init(DistCGArgs A) {
     }
 }
 
-__global__ void __launch_bounds__(NT, MSK_MINB) k_dcg_spmv(DistCGArgs A) {
+template <int C, int MB>
+__global__ void __launch_bounds__(NT, MB) k_dcg_spmv(DistCGArgs A) {
     if (!A.sc->active) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CGSharedT &S = *reinterpret_cast<CGSharedT *>(smem_raw);
+    CGSharedTT<C> &S = *reinterpret_cast<CGSharedTT<C> *>(smem_raw);
     if (threadIdx.x == 0) {
         for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_empty[b], NW);
         mbar_init(&S.bar_rp[0], 1);
         mbar_init(&S.bar_rp[1], 1);
         fence_mbar_init();
@@ -702,6 +754,7 @@ __global__ void __launch_bounds__(NT, 3) k_mf_spmv(DistCGArgs A, LevelView V) {
     const double d2 = V.delta2, inv = V.inv_delta, scl = V.scale;
     const float fthr = V.fthr;
     const float4 *__restrict__ frec = V.frec;
+    const double4 *__restrict__ rec = V.rec;
     for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x) {
         double dot = 0.0;
         for (int t = 0; t < CH; ++t) {
@@ -720,9 +773,8 @@ __global__ void __launch_bounds__(NT, 3) k_mf_spmv(DistCGArgs A, LevelView V) {
             auto flush = [&]() {
                 for (int h = 0; h < nh; ++h) {
                     const int j = hl[h];
-                    double y[3];
-#pragma unroll
-                    for (int a = 0; a < D; ++a) y[a] = V.x[a][j];
+                    const double4 R = rec[j];  // packed coordinates (the .w slot is unused here)
+                    const double y[3] = {R.x, R.y, R.z};
                     const double r2 = dist2_nofma<D>(x, y);
                     if (r2 < d2) {
                         const double v = scl * wendland<K>(sqrt(r2) * inv);
@@ -732,13 +784,22 @@ __global__ void __launch_bounds__(NT, 3) k_mf_spmv(DistCGArgs A, LevelView V) {
                 nh = 0;
             };
             for_each_range<D>(V, x, [&](int b, int e) {
-                for (int j = b; j < e; ++j) {
-                    const float4 F = frec[j];
-                    const float a0 = xf[0] - F.x, b0 = xf[1] - F.y, c0 = xf[2] - F.z;
-                    if (fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr) {
-                        if (nh == HM) flush();
-                        hl[nh++] = j;
-                    }
+                int j = b;
+                for (; j + 1 < e; j += 2) {  // two candidates per trip (independent loads)
+                    const float4 F0 = frec[j], F1 = frec[j + 1];
+                    const float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    const float a1 = xf[0] - F1.x, b1 = xf[1] - F1.y, c1 = xf[2] - F1.z;
+                    const bool h0 = fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr;
+                    const bool h1 = fmaf(c1, c1, fmaf(b1, b1, a1 * a1)) < fthr;
+                    if (nh + 2 > HM) flush();
+                    if (h0) hl[nh++] = j;
+                    if (h1) hl[nh++] = j + 1;
+                }
+                if (j < e) {
+                    const float4 F0 = frec[j];
+                    const float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    if (nh + 1 > HM) flush();
+                    if (fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr) hl[nh++] = j;
                 }
             });
             flush();
@@ -820,28 +881,42 @@ __global__ void k_col_minmax(int64_t nnz, const int32_t *__restrict__ col, unsig
     }
 }
 
-int g_max_resident = 0;
+// the two piece-capacity variants of k_cg / k_dcg_spmv
+struct CGVariant {
+    const void *cg, *dcg;
+    size_t smem;
+    int resident;  // co-resident CTAs of k_cg on the device
+};
+CGVariant g_var[2];
 
 void set_smem_attrs() {
     static bool done = false;
     if (done) return;
-    MSK_CUDA(cudaFuncSetAttribute(k_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGSharedT)));
+    g_var[0] = {(const void *)k_cg<CAPT0, MINB0>, (const void *)k_dcg_spmv<CAPT0, MINB0>,
+                sizeof(CGSharedTT<CAPT0>), 0};
+    g_var[1] = {(const void *)k_cg<CAPT1, MINB1>, (const void *)k_dcg_spmv<CAPT1, MINB1>,
+                sizeof(CGSharedTT<CAPT1>), 0};
+    int dev = 0, sms = 0;
+    MSK_CUDA(cudaGetDevice(&dev));
+    MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (auto &v : g_var) {
+        MSK_CUDA(cudaFuncSetAttribute(v.cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+        MSK_CUDA(cudaFuncSetAttribute(v.dcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+        int per = 0;
+        MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, v.cg, NT, v.smem));
+        v.resident = sms * (per > 0 ? per : 1);
+    }
     MSK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
-    MSK_CUDA(cudaFuncSetAttribute(k_dcg_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGSharedT)));
     done = true;
 }
+
+// variant by mean row length (entries per row of the work being launched)
+int cg_variant(double nnz, double rows) { return rows > 0 && nnz >= 16.0 * rows ? 1 : 0; }
 }  // namespace
 
 int cg_max_resident_blocks() {
-    if (g_max_resident == 0) {
-        set_smem_attrs();
-        int dev = 0, sms = 0, per = 0;
-        MSK_CUDA(cudaGetDevice(&dev));
-        MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg, NT, sizeof(CGSharedT)));
-        g_max_resident = sms * (per > 0 ? per : 1);
-    }
-    return g_max_resident;
+    set_smem_attrs();
+    return g_var[0].resident < g_var[1].resident ? g_var[0].resident : g_var[1].resident;
 }
 
 // tiles per chunk: a function of n only (keeps results launch-independent);
@@ -855,7 +930,11 @@ int cg_chunk_tiles(int64_t n) {
 void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     if (nlev <= 0) return;
     if (nlev > kMaxLevels) throw Error(1, "cg_batched: too many levels");
-    const int total = cg_max_resident_blocks();
+    set_smem_attrs();
+    double snnz = 0.0, srows = 0.0;
+    for (int l = 0; l < nlev; ++l) { snnz += (double)levels[l].nnz; srows += (double)levels[l].n; }
+    const CGVariant &var = g_var[cg_variant(snnz, srows)];
+    const int total = var.resident;
     if (total < nlev) throw Error(3, "cg_batched: fewer resident CTAs than levels");
     std::vector<double> work(nlev);
     double wsum = 0.0;
@@ -912,7 +991,7 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
         poff += 3 * nch[l];
     }
     void *args[] = {&B};
-    MSK_CUDA(cudaLaunchCooperativeKernel((void *)k_cg, dim3(used), dim3(NT), args, sizeof(CGSharedT), st));
+    MSK_CUDA(cudaLaunchCooperativeKernel(var.cg, dim3(used), dim3(NT), args, var.smem, st));
     if (launches) *launches += 1;
     MSK_CUDA(cudaFreeAsync(partials, st));
     MSK_CUDA(cudaFreeAsync(bars, st));
@@ -935,8 +1014,10 @@ void dcg_init(const DistCGArgs &a, cudaStream_t st) {
 }
 void dcg_spmv(const DistCGArgs &a, cudaStream_t st) {
     set_smem_attrs();
-    k_dcg_spmv<<<dcg_grid(a, 3), NT, sizeof(CGSharedT), st>>>(a);
-    MSK_CHECK_LAUNCH();
+    const double rows = (double)(a.c1 - a.c0) * a.L.chunk_tiles * NT;
+    const CGVariant &var = g_var[cg_variant((double)a.L.nnz, rows)];
+    void *args[] = {(void *)&a};
+    MSK_CUDA(cudaLaunchKernel(var.dcg, dim3(dcg_grid(a, 3)), dim3(NT), args, var.smem, st));
 }
 void dcg_rupd(const DistCGArgs &a, cudaStream_t st) {
     k_dcg_rupd<<<dcg_grid(a, 8), NT, 0, st>>>(a);

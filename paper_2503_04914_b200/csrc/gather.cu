@@ -26,8 +26,17 @@
 namespace msk {
 
 namespace {
-constexpr int NT = 256;
-constexpr int HMAX = 40;  // hit-list capacity per thread (flushed when full)
+#ifndef MSK_GNT
+#define MSK_GNT 256
+#endif
+#ifndef MSK_HMAX
+#define MSK_HMAX 40
+#endif
+#ifndef MSK_GMINB
+#define MSK_GMINB 4
+#endif
+constexpr int NT = MSK_GNT;
+constexpr int HMAX = MSK_HMAX;  // hit-list capacity per thread (flushed when full)
 
 template <int D>
 __device__ __forceinline__ double rec_dist2(const double *x, const double4 &R) {
@@ -41,7 +50,7 @@ __device__ __forceinline__ double rec_coef(const double4 &R) {
 }
 
 template <int D, int K>
-__global__ void __launch_bounds__(NT, 3) k_gather(GatherArgs a) {
+__global__ void __launch_bounds__(NT, MSK_GMINB) k_gather(GatherArgs a) {
     __shared__ long long sm[NT / 32 + 1];
     int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
     long long hits = 0;

@@ -38,6 +38,55 @@ __device__ __forceinline__ void for_each_range(const LevelView &L, const double 
     }
 }
 
+// The exact neighbours {j : r^2(x, x_j) < delta^2} (no-FMA r^2, reading C-4)
+// of x among cols' points, in ascending j: f(j, r2) per hit.  Candidates pass
+// a conservative FP32 prefilter on the 16-byte records cols.frec first (see
+// prefilter_threshold in gather.cu: it never rejects a true neighbour), the
+// survivors are buffered (HM per thread, keeps the warp convergent) and get
+// the exact FP64 test.  Requires cols.frec (relative to cols.g.lo).
+template <int D, int HM = 32, typename F>
+__device__ __forceinline__ void for_each_hit(const LevelView &cols, const double *x, F &&f) {
+    float xf[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) xf[a] = (float)(x[a] - cols.g.lo[a]);
+    const float fthr = cols.fthr;
+    const double d2 = cols.delta2;
+    const float4 *__restrict__ frec = cols.frec;
+    int hl[HM];
+    int nh = 0;
+    auto flush = [&]() {
+        for (int h = 0; h < nh; ++h) {
+            const int j = hl[h];
+            double y[3];
+#pragma unroll
+            for (int a = 0; a < D; ++a) y[a] = cols.x[a][j];
+            const double r2 = dist2_nofma<D>(x, y);
+            if (r2 < d2) f(j, r2);
+        }
+        nh = 0;
+    };
+    for_each_range<D>(cols, x, [&](int b, int e) {
+        int j = b;
+        for (; j + 1 < e; j += 2) {  // two candidates per trip (independent loads)
+            const float4 F0 = frec[j], F1 = frec[j + 1];
+            const float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+            const float a1 = xf[0] - F1.x, b1 = xf[1] - F1.y, c1 = xf[2] - F1.z;
+            const bool h0 = fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr;
+            const bool h1 = fmaf(c1, c1, fmaf(b1, b1, a1 * a1)) < fthr;
+            if (nh + 2 > HM) flush();
+            if (h0) hl[nh++] = j;
+            if (h1) hl[nh++] = j + 1;
+        }
+        if (j < e) {
+            const float4 F0 = frec[j];
+            const float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+            if (nh + 1 > HM) flush();
+            if (fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr) hl[nh++] = j;
+        }
+    });
+    flush();
+}
+
 // Same enumeration with a reach of m cells per axis (radius up to m cell
 // sides): used for the truncation radius T q_l of the thresholded factor,
 // which spans several cells of the level grid.
