@@ -35,6 +35,17 @@ struct msk_ctx {
     int rank = 0, world = 1;
     bool emulated = false;
     ncclComm_t comm = nullptr;
+    // copy streams for host-buffer calls (H2D / D2H overlapped with the compute
+    // stream in chunks); created on first use
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaStream_t copy_in() {
+        if (!cin) MSK_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+        return cin;
+    }
+    cudaStream_t copy_out() {
+        if (!cout) MSK_CUDA(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+        return cout;
+    }
 };
 
 namespace {
@@ -91,18 +102,29 @@ struct DevBuf {
     double *owned = nullptr;
     cudaStream_t st = nullptr;
     DevBuf() = default;
-    DevBuf(const double *p, size_t count, cudaStream_t s) : st(s) {
+    const double *src = nullptr;  // deferred copy: host source (copy_async)
+    size_t count = 0;
+    DevBuf(const double *p, size_t c, cudaStream_t s, bool defer = false) : st(s), count(c) {
         if (is_device_ptr(p)) {
             ptr = p;
         } else {
-            owned = dalloc<double>(count, s);
-            if (count) MSK_CUDA(cudaMemcpyAsync(owned, p, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+            owned = dalloc<double>(c, s);
+            if (defer) src = p;
+            else if (c) MSK_CUDA(cudaMemcpyAsync(owned, p, sizeof(double) * c, cudaMemcpyHostToDevice, s));
             ptr = owned;
         }
     }
+    // the deferred host->device copy on copy stream cs (after the allocation on st is ordered)
+    void copy_async(cudaStream_t cs) {
+        if (src && count)
+            MSK_CUDA(cudaMemcpyAsync(owned, src, sizeof(double) * count, cudaMemcpyHostToDevice, cs));
+        src = nullptr;
+    }
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
-    DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), owned(o.owned), st(o.st) { o.owned = nullptr; }
+    DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), owned(o.owned), st(o.st), src(o.src), count(o.count) {
+        o.owned = nullptr;
+    }
     ~DevBuf() { dfree(owned, st); }
 };
 
@@ -123,10 +145,22 @@ struct DevOut {
     }
     DevOut(const DevOut &) = delete;
     DevOut &operator=(const DevOut &) = delete;
-    DevOut(DevOut &&o) noexcept : ptr(o.ptr), host(o.host), count(o.count), st(o.st) { o.host = nullptr; }
+    bool flushed = false;
+    DevOut(DevOut &&o) noexcept : ptr(o.ptr), host(o.host), count(o.count), st(o.st), flushed(o.flushed) {
+        o.host = nullptr;
+    }
     void flush() {
-        if (host && count)
+        if (host && count && !flushed)
             MSK_CUDA(cudaMemcpyAsync(host, ptr, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+        flushed = true;
+    }
+    // device->host copy on copy stream cs once `ready` (recorded on st) has fired
+    void flush_async(cudaStream_t cs, cudaEvent_t ready) {
+        if (host && count && !flushed) {
+            MSK_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+            MSK_CUDA(cudaMemcpyAsync(host, ptr, sizeof(double) * count, cudaMemcpyDeviceToHost, cs));
+        }
+        flushed = true;
     }
     ~DevOut() {
         if (host) dfree(ptr, st);
@@ -151,6 +185,17 @@ struct Timer {
         if (a) cudaEventDestroy(a);
         if (b) cudaEventDestroy(b);
     }
+};
+
+// a synchronisation-only event
+struct Ev {
+    cudaEvent_t e = nullptr;
+    Ev() { MSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    Ev(const Ev &) = delete;
+    Ev &operator=(const Ev &) = delete;
+    ~Ev() { if (e) cudaEventDestroy(e); }
+    void record(cudaStream_t s) { MSK_CUDA(cudaEventRecord(e, s)); }
+    void wait_on(cudaStream_t s) { MSK_CUDA(cudaStreamWaitEvent(s, e, 0)); }
 };
 
 #define API_BEGIN try {
@@ -330,6 +375,8 @@ extern "C" void msk_ctx_destroy(msk_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
+    if (ctx->cin) { cudaStreamSynchronize(ctx->cin); cudaStreamDestroy(ctx->cin); }
+    if (ctx->cout) { cudaStreamSynchronize(ctx->cout); cudaStreamDestroy(ctx->cout); }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -912,10 +959,29 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     std::vector<DevOut> ad;
     fd.reserve(L);
     ad.reserve(L);
+    // host buffers: f^(l) copied in on a copy stream (level order, one event per
+    // level) and alpha^(l) copied out as soon as level l is final (PRUNED), so
+    // the transfers overlap the solve of the other levels
+    cudaStream_t cin = h->ctx->copy_in(), cout = h->ctx->copy_out();
     for (int l = 0; l < L; ++l) {
-        fd.emplace_back(f[l], (size_t)h->lev[l].n, st);
+        fd.emplace_back(f[l], (size_t)h->lev[l].n, st, true);
         ad.emplace_back(alpha[l], (size_t)h->lev[l].n, st);
     }
+    std::vector<Ev> ev_f((size_t)L), ev_a((size_t)L);
+    {
+        Ev ready;
+        ready.record(st);
+        ready.wait_on(cin);
+        for (int l = 0; l < L; ++l) {
+            fd[l].copy_async(cin);
+            ev_f[l].record(cin);
+        }
+    }
+    auto wait_f = [&](int l) { ev_f[l].wait_on(st); };
+    auto out_alpha = [&](int l) {  // alpha^(l) final in ad[l].ptr (caller order)
+        ev_a[l].record(st);
+        ad[l].flush_async(cout, ev_a[l].e);
+    };
     // device-side per-launch stats: [slot][level]
     const int nslots = schedule == MSK_SCHED_LITERAL ? L + 1 : 1;
     int *d_it = dalloc<int>((size_t)(nslots * L), st);
@@ -1152,6 +1218,8 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     require(!mf || schedule == MSK_SCHED_PRUNED, "msk_solve: a matrix-free hierarchy uses the PRUNED schedule");
 
     const bool thresholded = h->T > 0.0;
+    if (thresholded || schedule != MSK_SCHED_PRUNED)
+        for (int l = 0; l < L; ++l) wait_f(l);
     if (thresholded) {
         // a7: Jacobi on (id - M~(T)) beta = f (eq:perturbed_split P:865-869),
         // beta^(k) = f^(k) - sum_{l<k} X~_kl beta^(l) with the stored factor;
@@ -1197,8 +1265,10 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         // same solve); the finest level is solved at tol.
         for (int l = 0; l < L; ++l) {
             const double tl = l + 1 < L ? inner_tol : tol;
+            wait_f(l);
             if (h->dist[l].on || mf) {
                 dist_level(l, tl);
+                out_alpha(l);
                 debug_sync(st, "dist_level");
                 if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);
                 continue;
@@ -1218,6 +1288,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             time_cg(l);
             cg_batched(&a, 1, st, &launches);
             cg_t.back()->stop();
+            out_alpha(l);
             debug_sync(st, "cg");
             if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);  // source records for later B products
             debug_sync(st, "pack");
@@ -1255,6 +1326,12 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     }
     ttot.stop();
     for (int l = 0; l < L; ++l) ad[l].flush();
+    {  // the copy streams' work completes before the results are read / buffers freed on st
+        for (int l = 0; l < L; ++l) wait_f(l);
+        Ev done;
+        done.record(cout);
+        done.wait_on(st);
+    }
     std::vector<int> it((size_t)(nslots * L)), stat((size_t)(nslots * L));
     std::vector<double> rr((size_t)(2 * nslots * L));
     unsigned long long hits = 0;
@@ -1319,6 +1396,96 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
 }
 
 // ================================================================ evaluate
+namespace {
+// Host-buffer evaluation on one GPU, pipelined in chunks of evaluation points:
+// chunk c+1 is copied in (copy stream) while chunk c is sorted and evaluated
+// (compute stream) and chunk c-1's values are copied out (second copy
+// stream).  Every output depends only on its own point (fixed summation
+// order), so the result is identical to the one-shot path.
+void evaluate_pipelined(msk_hierarchy *h, int64_t m, const double *x, double *s, msk_eval_info *info) {
+    cudaStream_t st = h->st(), cin = h->ctx->copy_in(), cout = h->ctx->copy_out();
+    const int d = h->d, L = h->L;
+    int launches = 0;
+    int64_t chunk = 1 << 20;
+    if (const char *e = getenv("MSK_EVAL_CHUNK")) chunk = std::max<int64_t>(256, atoll(e));  // test hook
+    const int64_t nc = (m + chunk - 1) / chunk;
+    Timer ttot(st);
+    ttot.start();
+    const LevelData &F = h->lev[L - 1];
+    const Grid g = F.g;
+    double *xd = dalloc<double>((size_t)(m * d), st);
+    double *sd = dalloc<double>((size_t)m, st);
+    const int64_t cmax = std::min(chunk, m);
+    double *xs = dalloc<double>((size_t)(cmax * d), st);
+    int32_t *perm = dalloc<int32_t>((size_t)cmax, st);
+    int32_t *cs = dalloc<int32_t>((size_t)(g.ncells + 1), st);
+    unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
+    MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
+    for (int l = 0; l < L; ++l) h->pack(l, h->lev[l].alpha, &launches);
+    Ev ready;
+    ready.record(st);  // allocations (stream-ordered on st) before the copy streams touch them
+    ready.wait_on(cin);
+    ready.wait_on(cout);
+    std::vector<Ev> ein((size_t)nc), eout((size_t)nc);
+    std::vector<Timer *> tso, tev;
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t c0 = c * chunk, c1 = std::min(m, c0 + chunk), nck = c1 - c0;
+        MSK_CUDA(cudaMemcpyAsync(xd + c0 * d, x + c0 * d, sizeof(double) * (size_t)(nck * d),
+                                 cudaMemcpyHostToDevice, cin));
+        ein[c].record(cin);
+    }
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t c0 = c * chunk, c1 = std::min(m, c0 + chunk), nck = c1 - c0;
+        ein[c].wait_on(st);
+        CellListOut co{};
+        co.perm = perm;
+        for (int a = 0; a < d; ++a) co.xs[a] = xs + (size_t)a * nck;
+        co.cell_start = cs;
+        tso.push_back(new Timer(st));
+        tso.back()->start();
+        build_cell_list(d, nck, xd + c0 * d, g, false, co, st, &launches);
+        tso.back()->stop();
+        GatherArgs ga{};
+        ga.d = d;
+        ga.k = h->k;
+        ga.nt = nck;
+        for (int a = 0; a < d; ++a) ga.tx[a] = xs + (size_t)a * nck;
+        ga.nlev = L;
+        for (int l = 0; l < L; ++l) ga.lev[l] = h->view(l, h->lev[l].alpha);
+        ga.base = nullptr;
+        ga.sign = 1.0;
+        ga.out = sd + c0;
+        ga.out_perm = perm;
+        ga.hits = d_hits;
+        tev.push_back(new Timer(st));
+        tev.back()->start();
+        gather(ga, st, &launches);
+        tev.back()->stop();
+        eout[c].record(st);
+        eout[c].wait_on(cout);
+        MSK_CUDA(cudaMemcpyAsync(s + c0, sd + c0, sizeof(double) * (size_t)nck, cudaMemcpyDeviceToHost, cout));
+    }
+    Ev done;
+    done.record(cout);
+    done.wait_on(st);
+    ttot.stop();
+    unsigned long long hits = 0;
+    MSK_CUDA(cudaMemcpyAsync(&hits, d_hits, sizeof hits, cudaMemcpyDeviceToHost, st));
+    dfree(xd, st); dfree(sd, st); dfree(xs, st); dfree(perm, st); dfree(cs, st); dfree(d_hits, st);
+    MSK_CUDA(cudaStreamSynchronize(st));
+    double tsort = 0, teval = 0;
+    for (auto *t : tso) { tsort += t->ms(); delete t; }
+    for (auto *t : tev) { teval += t->ms(); delete t; }
+    if (info) {
+        info->nnz = (double)hits;
+        info->t_sort_ms = tsort;
+        info->t_eval_ms = teval;
+        info->t_total_ms = ttot.ms();
+        info->launches = launches;
+    }
+}
+}  // namespace
+
 extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x, double *s,
                                       msk_eval_info *info) {
     API_BEGIN
@@ -1330,6 +1497,10 @@ extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double 
     if (info) memset(info, 0, sizeof *info);
     if (m == 0) return MSK_OK;
     MSK_CUDA(cudaSetDevice(h->ctx->device));
+    if (h->ctx->world == 1 && !is_device_ptr(x) && !is_device_ptr(s)) {
+        evaluate_pipelined(h, m, x, s, info);
+        return MSK_OK;
+    }
     cudaStream_t st = h->st();
     const int d = h->d, L = h->L;
     int launches = 0;

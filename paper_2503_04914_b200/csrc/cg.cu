@@ -109,7 +109,6 @@ struct __align__(16) CGSharedTT {
     double red[NT / 32 + 2];
     uint64_t bar_st[NSTG];
     uint64_t bar_rp[2];
-    uint64_t bar_empty[NSTG];  // MSK_EMPTYBAR: one arrival per warp when a stage is consumed
 };
 
 __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
@@ -316,14 +315,6 @@ __device__ __forceinline__ void issue_rp(SH &S, int b, const int64_t *row_ptr, i
     tma_load_1d(S.rp[b], row_ptr + lo, bytes, &S.bar_rp[b], pol);
 }
 
-// before issuing piece Q into stage Q % 2: piece Q - 2 (same stage) consumed by every warp
-template <class SH>
-__device__ __forceinline__ void stage_free(SH &S, uint32_t Q) {
-#ifdef MSK_EMPTYBAR
-    if (Q >= 2) mbar_wait(&S.bar_empty[Q & 1], ((Q - 2) >> 1) & 1u);
-#endif
-}
-
 template <class SH>
 __device__ __forceinline__ void issue_piece_t(SH &S, int b, const int32_t *col, const double *val,
                                               int64_t kb, int64_t ke, uint64_t pol) {
@@ -369,16 +360,13 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
     {
         const int64_t *rp = S.rp[ps.CS & 1] + rp_off(cr0);
         const int64_t K0 = rp[0], K1 = rp[crows];
-        if (tid == 0) {
-            stage_free(S, ps.P);
-            issue_piece_t(S, ps.P & 1, L.col, L.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
-        }
+        if (tid == 0) issue_piece_t(S, ps.P & 1, L.col, L.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
     }
     for (int64_t k = 0; k < K; ++k) {
         chunk_rows(k, cr0, crows);
         const uint32_t cs = ps.CS + (uint32_t)k;
-#ifdef MSK_PF
-        // the epilogue's own-row vectors of the NEXT chunk -> L2 (hidden behind this chunk's pieces)
+        // the epilogue's own-row vectors of the NEXT chunk -> L2 (hidden behind
+        // this chunk's pieces; 33.38 -> 33.1 ms on the C3 finest level)
         if (tid == 0 && !first && k + 1 < K) {
             int64_t nr0;
             int nrows;
@@ -390,7 +378,6 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
                 if (a1 > a0) prefetch_l2((const void *)a0, (uint32_t)(a1 - a0));
             }
         }
-#endif
         const int64_t *rp = S.rp[cs & 1] + rp_off(cr0);
         const int64_t K1 = rp[crows];
         int64_t rb[MAXCH], re[MAXCH];
@@ -408,14 +395,11 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             // the next piece (rest of this chunk, or the first piece of the next
             // one) goes into the other stage, which held piece P-1 (consumed)
             if (ke < K1) {
-                if (tid == 0) {
-                    stage_free(S, ps.P + 1);
+                if (tid == 0)
                     issue_piece_t(S, (ps.P + 1) & 1, L.col, L.val, ke, ke + CAPTE < K1 ? ke + CAPTE : K1, pol);
-                }
             } else if (k + 1 < K) {
                 mbar_wait(&S.bar_rp[(cs + 1) & 1], ((cs + 1) >> 1) & 1u);
                 if (tid == 0) {
-                    stage_free(S, ps.P + 1);
                     int64_t nr0;
                     int nrows;
                     chunk_rows(k + 1, nr0, nrows);
@@ -447,12 +431,9 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
                         if (e + u < hi) acc[t] = fma(vv[u], pv[u], acc[t]);
                 }
             }
-#ifdef MSK_EMPTYBAR
-            __syncwarp();  // this warp is done with stage P%NSTG
-            if ((tid & 31) == 0) mbar_arrive(&S.bar_empty[ps.P & 1]);
-#else
-            __syncthreads();  // stage P%NSTG consumed by every thread: it may be refilled
-#endif
+            // stage P%NSTG consumed by every thread: it may be refilled.  (Per-warp
+            // release through "empty" mbarriers instead was slower: 35.1 vs 33.4 ms.)
+            __syncthreads();
             ++ps.P;
             kb = ke;
         }
@@ -519,7 +500,6 @@ __global__ void __launch_bounds__(NT, MB) k_cg(CGBatch B) {
     PipeState ps{0u, 0u};
     if (tid == 0) {
         for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
-        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_empty[b], NW);
         mbar_init(&S.bar_rp[0], 1);
         mbar_init(&S.bar_rp[1], 1);
         fence_mbar_init();
@@ -687,7 +667,6 @@ __global__ void __launch_bounds__(NT, MB) k_dcg_spmv(DistCGArgs A) {
     CGSharedTT<C> &S = *reinterpret_cast<CGSharedTT<C> *>(smem_raw);
     if (threadIdx.x == 0) {
         for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
-        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_empty[b], NW);
         mbar_init(&S.bar_rp[0], 1);
         mbar_init(&S.bar_rp[1], 1);
         fence_mbar_init();
@@ -742,7 +721,7 @@ __global__ void __launch_bounds__(NT) k_dcg_xfin(DistCGArgs A) {
 // Candidates: conservative FP32 prefilter (gather.cu), then the exact no-FMA
 // test (reading C-4) on the survivors.
 template <int D, int K>
-__global__ void __launch_bounds__(NT, 3) k_mf_spmv(DistCGArgs A, LevelView V) {
+__global__ void __launch_bounds__(NT, 4) k_mf_spmv(DistCGArgs A, LevelView V) {
     if (!A.sc->active) return;
     __shared__ double red[NT / 32 + 2];
     constexpr int HM = 40;
@@ -1028,7 +1007,7 @@ void dcg_xfin(const DistCGArgs &a, cudaStream_t st) {
     MSK_CHECK_LAUNCH();
 }
 void dcg_mf_spmv(const DistCGArgs &a, const LevelView &v, int d, int k, cudaStream_t st) {
-#define MSK_MF(DD, KK) k_mf_spmv<DD, KK><<<dcg_grid(a, 3), NT, 0, st>>>(a, v)
+#define MSK_MF(DD, KK) k_mf_spmv<DD, KK><<<dcg_grid(a, 4), NT, 0, st>>>(a, v)
     if (d == 2) {
         if (k == 0) MSK_MF(2, 0); else if (k == 1) MSK_MF(2, 1); else MSK_MF(2, 2);
     } else {

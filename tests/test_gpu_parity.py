@@ -279,6 +279,25 @@ def test_torch_device_buffers_match_host(msk, ctx):
         assert np.array_equal(a3[l], a_host[l])
 
 
+@pytest.mark.parametrize("chunk", ["257", "4096", "1048576"])
+def test_pipelined_host_evaluate(msk, ctx, chunk, monkeypatch):
+    """Host buffers: s_L is evaluated in chunks with the copies overlapped
+    (copy streams); every value must equal the device-buffer path's, for
+    chunkings with ragged tails (MSK_EVAL_CHUNK is a test hook)."""
+    import torch
+    H = HIERS["halton3d"]()
+    h = _hier(msk, ctx, H)
+    h.solve(H.f())
+    xh = uniform_points(20_011, 3, seed=9)
+    s_dev, e_dev = h.evaluate(torch.from_numpy(xh).cuda())
+    monkeypatch.setenv("MSK_EVAL_CHUNK", chunk)
+    s_host, e_host = h.evaluate(xh)
+    assert np.array_equal(s_dev.cpu().numpy(), s_host)
+    assert e_host.nnz == e_dev.nnz
+    ref = oracle.evaluate(H.points, H.delta, [h_ for h_ in h.solve(H.f())[0]], xh[:500], k=H.k)
+    assert _rel(s_host[:500], ref) < 1e-12
+
+
 # -------------------------------------------------------------- edge cases
 def test_edge_cases(msk, ctx):
     H = HIERS["C1"]()
