@@ -911,8 +911,17 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     if (nlev > kMaxLevels) throw Error(1, "cg_batched: too many levels");
     set_smem_attrs();
     double snnz = 0.0, srows = 0.0;
-    for (int l = 0; l < nlev; ++l) { snnz += (double)levels[l].nnz; srows += (double)levels[l].n; }
-    const CGVariant &var = g_var[cg_variant(snnz, srows)];
+    int64_t schunks = 0;
+    for (int l = 0; l < nlev; ++l) {
+        snnz += (double)levels[l].nnz;
+        srows += (double)levels[l].n;
+        const int64_t tiles = (levels[l].n + NT - 1) / NT, ch = cg_chunk_tiles(levels[l].n);
+        schunks += (tiles + ch - 1) / ch;
+    }
+    // long rows, or so few chunks that occupancy is moot: the large-piece
+    // variant (a small level's 256-row chunk then fits one piece)
+    const int vi = cg_variant(snnz, srows) == 1 || schunks <= g_var[1].resident ? 1 : 0;
+    const CGVariant &var = g_var[vi];
     const int total = var.resident;
     if (total < nlev) throw Error(3, "cg_batched: fewer resident CTAs than levels");
     std::vector<double> work(nlev);
