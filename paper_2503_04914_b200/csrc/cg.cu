@@ -94,8 +94,10 @@ struct __align__(16) CGShared {
 // C3 finest level 33.5 ms (2048) vs 37.7 (4096); C5 finest 1546 vs 1246 ms.
 constexpr int CAPT0 = MSK_CAPT;   // short-row variant
 constexpr int MINB0 = MSK_MINB;
-constexpr int CAPT1 = 4096;       // long-row variant
+constexpr int CAPT1 = 4096;       // long-row / few-chunk variant
 constexpr int MINB1 = 2;
+constexpr int CAPT2 = 2432;       // mid-size levels (one-tile chunks: 256 rows x ~9 entries fit one piece)
+constexpr int MINB2 = 3;
 constexpr int NSTG = 2;           // pipeline stages (NSTG - 1 pieces in flight ahead)
 template <int C>
 struct __align__(16) CtaStageT {
@@ -866,7 +868,7 @@ struct CGVariant {
     size_t smem;
     int resident;  // co-resident CTAs of k_cg on the device
 };
-CGVariant g_var[2];
+CGVariant g_var[3];
 
 void set_smem_attrs() {
     static bool done = false;
@@ -875,6 +877,8 @@ void set_smem_attrs() {
                 sizeof(CGSharedTT<CAPT0>), 0};
     g_var[1] = {(const void *)k_cg<CAPT1, MINB1>, (const void *)k_dcg_spmv<CAPT1, MINB1>,
                 sizeof(CGSharedTT<CAPT1>), 0};
+    g_var[2] = {(const void *)k_cg<CAPT2, MINB2>, (const void *)k_dcg_spmv<CAPT2, MINB2>,
+                sizeof(CGSharedTT<CAPT2>), 0};
     int dev = 0, sms = 0;
     MSK_CUDA(cudaGetDevice(&dev));
     MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -895,7 +899,9 @@ int cg_variant(double nnz, double rows) { return rows > 0 && nnz >= 16.0 * rows 
 
 int cg_max_resident_blocks() {
     set_smem_attrs();
-    return g_var[0].resident < g_var[1].resident ? g_var[0].resident : g_var[1].resident;
+    int r = g_var[0].resident;
+    for (const auto &v : g_var) r = v.resident < r ? v.resident : r;
+    return r;
 }
 
 // tiles per chunk: a function of n only (keeps results launch-independent);
@@ -912,15 +918,22 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     set_smem_attrs();
     double snnz = 0.0, srows = 0.0;
     int64_t schunks = 0;
+    int dom = 0;  // the level with the most work decides the chunk shape
     for (int l = 0; l < nlev; ++l) {
         snnz += (double)levels[l].nnz;
         srows += (double)levels[l].n;
         const int64_t tiles = (levels[l].n + NT - 1) / NT, ch = cg_chunk_tiles(levels[l].n);
         schunks += (tiles + ch - 1) / ch;
+        if (levels[l].nnz > levels[dom].nnz) dom = l;
     }
     // long rows, or so few chunks that occupancy is moot: the large-piece
-    // variant (a small level's 256-row chunk then fits one piece)
-    const int vi = cg_variant(snnz, srows) == 1 || schunks <= g_var[1].resident ? 1 : 0;
+    // variant (a small level's 256-row chunk then fits one piece); one-tile
+    // chunks of mid-size levels: 2432-entry pieces (one piece per chunk; C3
+    // levels 3/4 -12 %/-9 %); the finest levels (4-tile chunks) keep 2048, the
+    // larger smem carve-out costs them L1 for the gathers (+11 %).
+    int vi = 0;
+    if (cg_variant(snnz, srows) == 1 || schunks <= g_var[1].resident) vi = 1;
+    else if (cg_chunk_tiles(levels[dom].n) == 1) vi = 2;
     const CGVariant &var = g_var[vi];
     const int total = var.resident;
     if (total < nlev) throw Error(3, "cg_batched: fewer resident CTAs than levels");
