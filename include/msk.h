@@ -232,6 +232,27 @@ MSK_API msk_status msk_evaluate(msk_hierarchy *h, int64_t m, const double *x, do
 MSK_API msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x, double *s,
                            msk_eval_info *info);
 
+/* ------------------------------------------- multi-RHS */
+
+/* Solve the multiscale system (eq:mas P:284-290, PRUNED schedule as msk_solve)
+ * for nrhs right-hand sides at once.  f[l]: n[l] x nrhs row-major (f[l][i*nrhs
+ * + r] = sample of function r at x_i^(l)), [host] or [dev]; alpha[l]: n[l] x
+ * nrhs, caller-owned, same layout.  Columns are processed in groups of 4 (the
+ * tail 2 or 4, zero-padded): every CSR piece and every kernel evaluation of the
+ * B products serves the whole group, so the HBM traffic per right-hand side
+ * falls.  Every column is bit-identical to msk_solve with that column alone.
+ * iters: nullable, [L * nrhs] (iters[l*nrhs + r]).  t_ms: nullable, device
+ * time.  Requirements: exact mode (msk_assemble with T <= 0), assembled A_l (not
+ * MSK_FLAG_MATRIX_FREE), one GPU (world 1), else MSK_ERR_INVALID.  Keeps the
+ * coefficients for msk_evaluate_multi.  MSK_ERR_NOCONV names level and rhs. */
+MSK_API msk_status msk_solve_multi(msk_hierarchy *h, int32_t nrhs, const double *const *f, double tol,
+                           int32_t max_iter, double *const *alpha, int32_t *iters, double *t_ms);
+
+/* s[i*nrhs + r] = f_L of right-hand side r at x_i (eq:fapproximation P:293-296)
+ * from the last msk_solve_multi; x: m x d, s: m x nrhs ([host] or [dev]).
+ * MSK_ERR_STATE before msk_solve_multi. */
+MSK_API msk_status msk_evaluate_multi(msk_hierarchy *h, int64_t m, const double *x, double *s);
+
 /* ----------------------------------------- row-level entry points (tests) */
 
 /* Sparsity pattern (and optionally values) of block B_{row_level,col_level}

@@ -111,6 +111,19 @@ def msk_solve(h, f, tol, max_iter, schedule, alpha):
     return info
 
 
+def msk_solve_multi(h, nrhs, f, tol, max_iter, alpha, iters=None):
+    """iters: optional int32 array [L * nrhs]; returns the device time (ms)."""
+    fp, k1 = _ptr_array(f)
+    ap, k2 = _ptr_array(alpha)
+    t = ctypes.c_double(0.0)
+    check(load().msk_solve_multi(h, int(nrhs), fp, float(tol), int(max_iter), ap, _ptr(iters), ctypes.byref(t)))
+    return t.value
+
+
+def msk_evaluate_multi(h, m, x, s):
+    check(load().msk_evaluate_multi(h, int(m), _ptr(x), _ptr(s)))
+
+
 def msk_evaluate(h, m, x, s):
     check(load().msk_evaluate(h, int(m), _ptr(x), _ptr(s)))
 
@@ -269,6 +282,35 @@ class Hierarchy:
         info = msk_solve(self.handle, f, tol, max_iter, sch, alpha)
         self.last_solve = info
         return alpha, info
+
+    def solve_multi(self, F, tol=1e-12, max_iter=20000):
+        """F: per level an (n_l, nrhs) array (numpy or CUDA tensor).  Returns
+        (alpha list of (n_l, nrhs), iterations (L, nrhs), device ms)."""
+        F = [_f64(x) for x in F]
+        nrhs = int(F[0].shape[1]) if len(F[0].shape) == 2 else 1
+        alpha = []
+        for l in range(self.L):
+            if _is_torch(F[l]):
+                import torch
+                alpha.append(torch.empty((self.n[l], nrhs), dtype=torch.float64, device=F[l].device))
+            else:
+                alpha.append(np.empty((self.n[l], nrhs), dtype=np.float64))
+        iters = np.zeros(self.L * nrhs, dtype=np.int32)
+        t = msk_solve_multi(self.handle, nrhs, F, tol, max_iter, alpha, iters)
+        self.nrhs = nrhs
+        return alpha, iters.reshape(self.L, nrhs), t
+
+    def evaluate_multi(self, x):
+        x = _f64(x)
+        m = int(x.shape[0])
+        nrhs = getattr(self, "nrhs", 1)  # before solve_multi the library reports MSK_ERR_STATE
+        if _is_torch(x):
+            import torch
+            s = torch.empty((m, nrhs), dtype=torch.float64, device=x.device)
+        else:
+            s = np.empty((m, nrhs), dtype=np.float64)
+        msk_evaluate_multi(self.handle, m, x, s)
+        return s
 
     def evaluate(self, x, out=None):
         x = _f64(x)

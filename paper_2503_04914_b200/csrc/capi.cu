@@ -230,6 +230,11 @@ struct msk_hierarchy {
     int64_t ntot = 0;
     int64_t off[kMaxLevels + 1] = {0};
     double *ws = nullptr;  // CG workspace: r, p, q, beta, t (5 * ntot)
+    // multi-RHS solve (msk_solve_multi): coefficients of all right-hand sides,
+    // spatial order, [n(l)][nrhs_pad] per level (columns grouped by 2 / 4)
+    double *alpham[kMaxLevels] = {nullptr};
+    int nrhs_m = 0, nrhs_pad = 0;
+    std::vector<int> grp0, grpR, grpP;  // caller column, width R, padded column of each group
     double t_create_ms = 0, t_assemble_ms = 0;
     int launches_create = 0, launches_assemble = 0;
     // thresholded factor M~(T) (a6): one CSR over all points (rows of level 1
@@ -321,8 +326,17 @@ struct msk_hierarchy {
         }
         dfree(ws, s);
         ws = nullptr;
+        release_multi();
         release_factor();
         release_dist();
+    }
+    void release_multi() {
+        for (int l = 0; l < kMaxLevels; ++l) {
+            dfree(alpham[l], st());
+            alpham[l] = nullptr;
+        }
+        nrhs_m = nrhs_pad = 0;
+        grp0.clear(); grpR.clear(); grpP.clear();
     }
 };
 
@@ -1563,6 +1577,203 @@ extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double 
         info->t_total_ms = ttot.ms();
         info->launches = launches;
     }
+    API_END
+}
+
+// ============================================================ multi-RHS
+// NEXT-3: several right-hand sides f_1..f_nrhs on the same
+// hierarchy (exact mode, PRUNED schedule, one GPU, assembled A_l).  Columns are
+// solved in groups of 4 (or 2): each CSR piece and each kernel evaluation of
+// the B products serves the whole group.  Per column the arithmetic is that of
+// msk_solve -- every column is bit-identical to its single-RHS solve.
+extern "C" msk_status msk_solve_multi(msk_hierarchy *h, int32_t nrhs, const double *const *f, double tol,
+                                      int32_t max_iter, double *const *alpha, int32_t *iters, double *t_ms) {
+    API_BEGIN
+    require(h && f && alpha, "msk_solve_multi: NULL argument");
+    require(nrhs >= 1 && nrhs <= 1024, "msk_solve_multi: nrhs must be in [1, 1024]");
+    require(tol > 0.0 && tol < 1.0 && max_iter >= 1, "msk_solve_multi: bad tol / max_iter");
+    if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_solve_multi: call msk_assemble first");
+    require(!(h->T > 0.0), "msk_solve_multi: exact mode only (msk_assemble with T <= 0)");
+    require(!(h->flags & MSK_FLAG_MATRIX_FREE), "msk_solve_multi: needs assembled A_l");
+    require(h->ctx->world == 1, "msk_solve_multi: single GPU in this version");
+    for (int l = 0; l < h->L; ++l) require(f[l] && alpha[l], "msk_solve_multi: NULL level pointer");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const int L = h->L;
+    const double inner_tol = tol / 10.0;  // reading C-10
+    h->release_multi();
+    // column groups: 4 wide, the tail 2 or 4 wide (padded with zero columns)
+    for (int c = 0, pc = 0; c < nrhs;) {
+        const int rem = nrhs - c, R = rem >= 3 ? 4 : 2;
+        h->grp0.push_back(c);
+        h->grpR.push_back(R);
+        h->grpP.push_back(pc);
+        c += std::min(R, rem);
+        pc += R;
+        h->nrhs_pad = pc;
+    }
+    h->nrhs_m = nrhs;
+    const int NP = h->nrhs_pad;
+    std::vector<DevBuf> fd;
+    std::vector<DevOut> ad;
+    fd.reserve(L);
+    ad.reserve(L);
+    for (int l = 0; l < L; ++l) {
+        fd.emplace_back(f[l], (size_t)(h->lev[l].n * nrhs), st);
+        ad.emplace_back(alpha[l], (size_t)(h->lev[l].n * nrhs), st);
+        h->alpham[l] = dalloc<double>((size_t)(h->lev[l].n * NP), st);
+    }
+    // workspace: r, p, q, beta per level for one group (R <= 4 columns)
+    double *wsm = dalloc<double>((size_t)(4 * 4 * h->ntot), st);
+    auto wsv = [&](int which, int l, int R) { return wsm + (size_t)which * 4 * h->ntot + (size_t)h->off[l] * R; };
+    for (int l = 0; l < L; ++l) h->pack(l, wsm, nullptr);  // packed coordinates for the B products
+    const int ng = (int)h->grp0.size();
+    int *d_it = dalloc<int>((size_t)(4 * L * ng), st);
+    int *d_stat = dalloc<int>((size_t)(4 * L * ng), st);
+    double *d_rr = dalloc<double>((size_t)(8 * L * ng), st);
+    MSK_CUDA(cudaMemsetAsync(d_it, 0, sizeof(int) * 4 * L * ng, st));
+    MSK_CUDA(cudaMemsetAsync(d_stat, 0, sizeof(int) * 4 * L * ng, st));
+    Timer tm(st);
+    tm.start();
+    int launches = 0;
+    for (int g = 0; g < ng; ++g) {
+        const int R = h->grpR[g], c0 = h->grp0[g], pc = h->grpP[g];
+        const int nvalid = std::min(R, nrhs - c0);
+        for (int l = 0; l < L; ++l) {
+            const LevelData &D = h->lev[l];
+            const double tl = l + 1 < L ? inner_tol : tol;
+            CGRArgs a{};
+            a.n = D.n;
+            a.nnz = D.nnz;
+            a.row_ptr = D.row_ptr;
+            a.col = D.col;
+            a.val = D.val;
+            a.ldb = nrhs;
+            a.col0 = c0;
+            a.nvalid = nvalid;
+            if (l == 0) {
+                a.b_src = fd[0].ptr;
+                a.b_perm = D.perm;
+            } else {
+                GatherMArgs ga{};
+                ga.d = h->d;
+                ga.k = h->k;
+                ga.R = R;
+                ga.nt = D.n;
+                for (int t = 0; t < h->d; ++t) ga.tx[t] = D.xs + (size_t)t * D.n;
+                ga.nlev = l;
+                for (int k = 0; k < l; ++k) {
+                    ga.lev[k] = h->view(k);
+                    ga.coef[k] = h->alpham[k] + pc;
+                }
+                ga.ldc = NP;
+                ga.base = fd[l].ptr;
+                ga.base_perm = D.perm;
+                ga.ldb = nrhs;
+                ga.bcol0 = c0;
+                ga.bcols = nvalid;
+                ga.sign = -1.0;
+                ga.out = wsv(3, l, R);
+                ga.out_perm = nullptr;
+                ga.ldo = R;
+                ga.ocol0 = 0;
+                ga.wcols = R;
+                gather_multi(ga, st, &launches);
+                a.b = wsv(3, l, R);
+            }
+            a.x = h->alpham[l] + pc;
+            a.ldx = NP;
+            a.r = wsv(0, l, R);
+            a.p = wsv(1, l, R);
+            a.q = wsv(2, l, R);
+            a.x_out = ad[l].ptr;
+            a.x_perm = D.perm;
+            a.ldo = nrhs;
+            a.tol2 = tl * tl;
+            a.max_iter = max_iter;
+            const int slot = (g * L + l) * 4;
+            a.out_iters = d_it + slot;
+            a.out_rr = d_rr + 2 * slot;
+            a.out_status = d_stat + slot;
+            cg_multi(a, R, st, &launches);
+        }
+    }
+    tm.stop();
+    for (int l = 0; l < L; ++l) ad[l].flush();
+    std::vector<int> hit((size_t)(4 * L * ng)), hst((size_t)(4 * L * ng));
+    std::vector<double> hrr((size_t)(8 * L * ng));
+    MSK_CUDA(cudaMemcpyAsync(hit.data(), d_it, sizeof(int) * hit.size(), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(hst.data(), d_stat, sizeof(int) * hst.size(), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(hrr.data(), d_rr, sizeof(double) * hrr.size(), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(wsm, st); dfree(d_it, st); dfree(d_stat, st); dfree(d_rr, st);
+    if (t_ms) *t_ms = tm.ms();
+    std::string noconv;
+    for (int g = 0; g < ng; ++g)
+        for (int l = 0; l < L; ++l)
+            for (int k = 0; k < std::min(h->grpR[g], nrhs - h->grp0[g]); ++k) {
+                const int slot = (g * L + l) * 4 + k, col = h->grp0[g] + k;
+                if (iters) iters[(size_t)l * nrhs + col] = hit[slot];
+                if (hst[slot] && noconv.empty()) {
+                    char buf[200];
+                    snprintf(buf, sizeof buf, "level %d, rhs %d: rel. residual %.3e after %d iterations", l, col,
+                             hrr[2 * slot + 1] > 0 ? sqrt(hrr[2 * slot] / hrr[2 * slot + 1]) : 0.0, hit[slot]);
+                    noconv = buf;
+                }
+            }
+    if (!noconv.empty()) throw Error(MSK_ERR_NOCONV, noconv);
+    API_END
+}
+
+// s[i][r] = f_L of right-hand side r at x_i (after msk_solve_multi); s is m x nrhs
+extern "C" msk_status msk_evaluate_multi(msk_hierarchy *h, int64_t m, const double *x, double *s) {
+    API_BEGIN
+    require(h != nullptr, "msk_evaluate_multi: NULL hierarchy");
+    require(m >= 0 && m < (1ll << 31) - 1, "msk_evaluate_multi: bad m");
+    require(m == 0 || (x && s), "msk_evaluate_multi: NULL argument");
+    if (h->nrhs_m == 0) throw Error(MSK_ERR_STATE, "msk_evaluate_multi: call msk_solve_multi first");
+    if (m == 0) return MSK_OK;
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const int d = h->d, L = h->L, nrhs = h->nrhs_m;
+    DevBuf xd(x, (size_t)(m * d), st);
+    DevOut sd(s, (size_t)(m * nrhs), st);
+    const LevelData &F = h->lev[L - 1];
+    const Grid g = F.g;
+    double *xs = dalloc<double>((size_t)(m * d), st);
+    int32_t *perm = dalloc<int32_t>((size_t)m, st);
+    int32_t *cs = dalloc<int32_t>((size_t)(g.ncells + 1), st);
+    CellListOut co{};
+    co.perm = perm;
+    for (int a = 0; a < d; ++a) co.xs[a] = xs + (size_t)a * m;
+    co.cell_start = cs;
+    build_cell_list(d, m, xd.ptr, g, false, co, st, nullptr);
+    for (int l = 0; l < L; ++l) h->pack(l, h->alpham[l], nullptr);  // coordinates (the .w slot is unused)
+    for (size_t gi = 0; gi < h->grp0.size(); ++gi) {
+        GatherMArgs ga{};
+        ga.d = d;
+        ga.k = h->k;
+        ga.R = h->grpR[gi];
+        ga.nt = m;
+        for (int a = 0; a < d; ++a) ga.tx[a] = xs + (size_t)a * m;
+        ga.nlev = L;
+        for (int l = 0; l < L; ++l) {
+            ga.lev[l] = h->view(l);
+            ga.coef[l] = h->alpham[l] + h->grpP[gi];
+        }
+        ga.ldc = h->nrhs_pad;
+        ga.base = nullptr;
+        ga.sign = 1.0;
+        ga.out = sd.ptr;
+        ga.out_perm = perm;
+        ga.ldo = nrhs;
+        ga.ocol0 = h->grp0[gi];
+        ga.wcols = std::min(h->grpR[gi], nrhs - h->grp0[gi]);
+        gather_multi(ga, st, nullptr);
+    }
+    sd.flush();
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(xs, st); dfree(perm, st); dfree(cs, st);
     API_END
 }
 

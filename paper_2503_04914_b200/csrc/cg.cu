@@ -607,6 +607,305 @@ __global__ void __launch_bounds__(NT, MB) k_cg(CGBatch B) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-RHS CG (msk_solve_multi): one level, R right-hand sides sharing every
+// CSR piece (the matrix is streamed once per iteration for all R columns).
+// Per column the arithmetic is k_cg's, in the same order (chunk partials,
+// block_sum tree, fma order in the rows), with per-column scalars; a column
+// that has met its stopping rule is frozen (alpha = beta = 0 from then on:
+// x, r unchanged exactly), so every column equals its single-RHS solve bit for
+// bit.  Vectors are [n][R] row-major (x with row stride ldx).
+template <int C, int R>
+struct __align__(16) CGSharedR {
+    CGSharedTT<C> b;
+    double redr[R * (NT / 32 + 1)];
+};
+
+template <int R>
+__device__ __forceinline__ void chunk_allreduce_r(const double *partials, int64_t nchunks, int nb,
+                                                  unsigned long long *ctr, unsigned long long &round,
+                                                  double *s_red, double (&out)[R]) {
+    group_barrier(ctr, nb, round);
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[r] = 0.0;
+    for (int64_t j = threadIdx.x; j < nchunks; j += NT) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[r] += __ldcg(&partials[j * R + r]);
+    }
+    block_sum_r<NT, R>(out, s_red);
+}
+
+template <int C, int R>
+__device__ __forceinline__ void spmv_phase_r(CGSharedR<C, R> &SR, const CGRArgs &A, int me, int nb, int CH,
+                                             double *part_out, PipeState &ps, uint64_t pol, bool first,
+                                             const double (&alpha_prev)[R], const double (&beta)[R]) {
+    constexpr int CAPTE = C - 2;
+    constexpr int UR = 2;  // gathers (R doubles each) in flight per thread
+    CGSharedTT<C> &S = SR.b;
+    const int tid = threadIdx.x;
+    const int64_t n = A.n;
+    const int64_t ntiles = (n + NT - 1) / NT, nloc = (ntiles + CH - 1) / CH;
+    const int64_t K = me < nloc ? (nloc - 1 - me) / nb + 1 : 0;
+    if (K == 0) return;
+    const double *rv = A.r;
+    auto chunk_rows = [&](int64_t k, int64_t &cr0, int &crows) {
+        const int64_t c = me + k * nb;
+        cr0 = c * CH * NT;
+        crows = (int)(n - cr0 < (int64_t)CH * NT ? n - cr0 : (int64_t)CH * NT);
+    };
+    auto rp_off = [&](int64_t cr0) { return (int)(cr0 - (cr0 & ~(int64_t)1)); };
+    int64_t cr0;
+    int crows;
+    if (tid == 0) {
+        chunk_rows(0, cr0, crows);
+        issue_rp(S, ps.CS & 1, A.row_ptr, cr0, crows, pol);
+        if (K > 1) {
+            chunk_rows(1, cr0, crows);
+            issue_rp(S, (ps.CS + 1) & 1, A.row_ptr, cr0, crows, pol);
+        }
+    }
+    mbar_wait(&S.bar_rp[ps.CS & 1], (ps.CS >> 1) & 1u);
+    chunk_rows(0, cr0, crows);
+    {
+        const int64_t *rp = S.rp[ps.CS & 1] + rp_off(cr0);
+        const int64_t K0 = rp[0], K1 = rp[crows];
+        if (tid == 0) issue_piece_t(S, ps.P & 1, A.col, A.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
+    }
+    for (int64_t k = 0; k < K; ++k) {
+        chunk_rows(k, cr0, crows);
+        const uint32_t cs = ps.CS + (uint32_t)k;
+        const int64_t *rp = S.rp[cs & 1] + rp_off(cr0);
+        const int64_t K1 = rp[crows];
+        int64_t rb[MAXCH], re[MAXCH];
+        double acc[MAXCH][R];
+#pragma unroll
+        for (int t = 0; t < MAXCH; ++t) {
+            const int r = t * NT + tid;
+            const bool ok = t < CH && r < crows;
+            rb[t] = ok ? rp[r] : 0;
+            re[t] = ok ? rp[r + 1] : 0;
+#pragma unroll
+            for (int c = 0; c < R; ++c) acc[t][c] = 0.0;
+        }
+        for (int64_t kb = rp[0]; kb < K1;) {
+            const int64_t ke = kb + CAPTE < K1 ? kb + CAPTE : K1;
+            if (ke < K1) {
+                if (tid == 0)
+                    issue_piece_t(S, (ps.P + 1) & 1, A.col, A.val, ke, ke + CAPTE < K1 ? ke + CAPTE : K1, pol);
+            } else if (k + 1 < K) {
+                mbar_wait(&S.bar_rp[(cs + 1) & 1], ((cs + 1) >> 1) & 1u);
+                if (tid == 0) {
+                    int64_t nr0;
+                    int nrows;
+                    chunk_rows(k + 1, nr0, nrows);
+                    const int64_t *nrp = S.rp[(cs + 1) & 1] + rp_off(nr0);
+                    const int64_t a = nrp[0], e = nrp[nrows];
+                    issue_piece_t(S, (ps.P + 1) & 1, A.col, A.val, a, a + CAPTE < e ? a + CAPTE : e, pol);
+                }
+            }
+            mbar_wait(&S.bar_st[ps.P & 1], (ps.P >> 1) & 1u);
+            const CtaStageT<C> &cur = S.st[ps.P & 1];
+            const int voff = (int)(kb & 1), coff = (int)(kb & 3);
+#pragma unroll
+            for (int t = 0; t < MAXCH; ++t) {
+                if (t >= CH) break;
+                const int64_t lo64 = rb[t] > kb ? rb[t] : kb, hi64 = re[t] < ke ? re[t] : ke;
+                const int lo = (int)(lo64 - kb);
+                const int hi = hi64 > lo64 ? (int)(hi64 - kb) : lo;
+                for (int e = lo; e < hi; e += UR) {
+                    double pv[UR][R], vv[UR];
+#pragma unroll
+                    for (int u = 0; u < UR; ++u) {
+                        const int ee = e + u;
+                        const bool ok = ee < hi;
+                        const double2 *src = reinterpret_cast<const double2 *>(rv + (int64_t)(ok ? cur.col[coff + ee] : 0) * R);
+#pragma unroll
+                        for (int c = 0; c < R; c += 2) {
+                            const double2 w2 = ok ? src[c / 2] : make_double2(0.0, 0.0);
+                            pv[u][c] = w2.x;
+                            pv[u][c + 1] = w2.y;
+                        }
+                        vv[u] = ok ? cur.val[voff + ee] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < UR; ++u)
+                        if (e + u < hi) {
+#pragma unroll
+                            for (int c = 0; c < R; ++c) acc[t][c] = fma(vv[u], pv[u][c], acc[t][c]);
+                        }
+                }
+            }
+            __syncthreads();
+            ++ps.P;
+            kb = ke;
+        }
+        double dot[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) dot[c] = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXCH; ++t) {
+            const int r = t * NT + tid;
+            if (t < CH && r < crows) {
+                const int64_t i = cr0 + r;
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    const double ri = rv[i * R + c];
+                    const double po = first ? 0.0 : A.p[i * R + c];
+                    const double qo = first ? 0.0 : A.q[i * R + c];
+                    const double xo = first ? 0.0 : A.x[i * A.ldx + c];
+                    const double pn = first ? ri : ri + beta[c] * po;
+                    const double qn = first ? acc[t][c] : acc[t][c] + beta[c] * qo;
+                    A.p[i * R + c] = pn;
+                    A.q[i * R + c] = qn;
+                    A.x[i * A.ldx + c] = first ? 0.0 : xo + alpha_prev[c] * po;
+                    dot[c] += pn * qn;
+                }
+            }
+        }
+        block_sum_r<NT, R>(dot, SR.redr);
+        if (tid == 0) {
+            const int64_t c0 = me + k * nb;
+#pragma unroll
+            for (int c = 0; c < R; ++c) part_out[c0 * R + c] = dot[c];
+            if (k + 2 < K) {
+                int64_t nr0;
+                int nrows;
+                chunk_rows(k + 2, nr0, nrows);
+                issue_rp(S, cs & 1, A.row_ptr, nr0, nrows, pol);
+            }
+        }
+    }
+    ps.CS += (uint32_t)K;
+}
+
+template <int C, int MB, int R>
+__global__ void __launch_bounds__(NT, MB) k_cgr(CGRArgs A, int nb, int CH, double *part,
+                                                unsigned long long *barrier) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CGSharedR<C, R> &SR = *reinterpret_cast<CGSharedR<C, R> *>(smem_raw);
+    CGSharedTT<C> &S = SR.b;
+    const int me = (int)blockIdx.x, tid = threadIdx.x;
+    const int64_t n = A.n;
+    const int64_t ntiles = (n + NT - 1) / NT;
+    const int64_t nchunks = (ntiles + CH - 1) / CH;
+    unsigned long long round = 0;
+    PipeState ps{0u, 0u};
+    if (tid == 0) {
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        mbar_init(&S.bar_rp[0], 1);
+        mbar_init(&S.bar_rp[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    // ---- init: r = b, bb = b.b per column
+    for (int64_t c = me; c < nchunks; c += nb) {
+        double acc[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = 0.0;
+        for (int t = 0; t < CH; ++t) {
+            const int64_t i = (c * CH + t) * NT + tid;
+            if (i < n) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    double bi;
+                    if (A.b) bi = __ldg(&A.b[i * R + k]);
+                    else bi = k < A.nvalid ? __ldg(&A.b_src[(int64_t)__ldg(&A.b_perm[i]) * A.ldb + A.col0 + k]) : 0.0;
+                    A.r[i * R + k] = bi;
+                    acc[k] += bi * bi;
+                }
+            }
+        }
+        block_sum_r<NT, R>(acc, SR.redr);
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) part[c * R + k] = acc[k];
+        }
+    }
+    double bb[R], rr[R], alpha[R], beta[R];
+    chunk_allreduce_r<R>(part, nchunks, nb, barrier, round, SR.redr, bb);
+    int itc[R];
+    bool act[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        rr[k] = bb[k];
+        alpha[k] = 0.0;
+        beta[k] = 0.0;
+        itc[k] = 0;
+    }
+    int it = 0;
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            act[k] = bb[k] > 0.0 && rr[k] > A.tol2 * bb[k] && it < A.max_iter;
+            any = any || act[k];
+        }
+        if (!any) break;
+        // ---- pass 1: w = A r ; p, q, x updates ; pq
+        spmv_phase_r<C, R>(SR, A, me, nb, CH, part + nchunks * R, ps, pol, it == 0, alpha, beta);
+        double pq[R];
+        chunk_allreduce_r<R>(part + nchunks * R, nchunks, nb, barrier, round, SR.redr, pq);
+#pragma unroll
+        for (int k = 0; k < R; ++k) alpha[k] = act[k] ? rr[k] / pq[k] : 0.0;
+        // ---- pass 2: r -= alpha q ; rr
+        for (int64_t c = me; c < nchunks; c += nb) {
+            double acc[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[k] = 0.0;
+            for (int t = 0; t < CH; ++t) {
+                const int64_t i = (c * CH + t) * NT + tid;
+                if (i < n) {
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const double ri = A.r[i * R + k] - alpha[k] * A.q[i * R + k];
+                        A.r[i * R + k] = ri;
+                        acc[k] += ri * ri;
+                    }
+                }
+            }
+            block_sum_r<NT, R>(acc, SR.redr);
+            if (tid == 0) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) part[(2 * nchunks + c) * R + k] = acc[k];
+            }
+        }
+        double rrn[R];
+        chunk_allreduce_r<R>(part + 2 * nchunks * R, nchunks, nb, barrier, round, SR.redr, rrn);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            beta[k] = act[k] ? rrn[k] / rr[k] : 0.0;
+            if (act[k]) {
+                rr[k] = rrn[k];
+                ++itc[k];
+            }
+        }
+        ++it;
+    }
+    // ---- the last deferred x update, then caller order
+    for (int64_t c = me; c < nchunks; c += nb)
+        for (int t = 0; t < CH; ++t) {
+            const int64_t i = (c * CH + t) * NT + tid;
+            if (i < n) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const double xi = it > 0 ? A.x[i * A.ldx + k] + alpha[k] * A.p[i * R + k] : 0.0;
+                    A.x[i * A.ldx + k] = xi;
+                    if (A.x_out && k < A.nvalid) A.x_out[(int64_t)__ldg(&A.x_perm[i]) * A.ldo + A.col0 + k] = xi;
+                }
+            }
+        }
+    if (me == 0 && tid == 0) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            A.out_iters[k] = itc[k];
+            A.out_rr[2 * k] = rr[k];
+            A.out_rr[2 * k + 1] = bb[k];
+            A.out_status[k] = bb[k] > 0.0 && rr[k] > A.tol2 * bb[k] ? 1 : 0;
+        }
+    }
+}
+
 // standalone y = A v (msk_apply_block): one CTA per tile
 __global__ void __launch_bounds__(NT) k_spmv(int64_t n, const int64_t *__restrict__ row_ptr,
                                              const int32_t *__restrict__ col,
@@ -996,6 +1295,39 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     if (launches) *launches += 1;
     MSK_CUDA(cudaFreeAsync(partials, st));
     MSK_CUDA(cudaFreeAsync(bars, st));
+}
+
+void cg_multi(const CGRArgs &a, int R, cudaStream_t st, int *launches) {
+    if (a.n == 0) return;
+    if (R != 2 && R != 4) throw Error(1, "cg_multi: R must be 2 or 4");
+    constexpr int CM = 2048;
+    const void *fn = R == 2 ? (const void *)k_cgr<CM, 2, 2> : (const void *)k_cgr<CM, 2, 4>;
+    const size_t smem = R == 2 ? sizeof(CGSharedR<CM, 2>) : sizeof(CGSharedR<CM, 4>);
+    static bool attr[2] = {false, false};
+    if (!attr[R == 4]) {
+        MSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[R == 4] = true;
+    }
+    int dev = 0, sms = 0, per = 0;
+    MSK_CUDA(cudaGetDevice(&dev));
+    MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, NT, smem));
+    const int CH = cg_chunk_tiles(a.n);
+    const int64_t nch = ((a.n + NT - 1) / NT + CH - 1) / CH;
+    int nb = sms * (per > 0 ? per : 1);
+    if (nb > nch) nb = (int)nch;
+    double *part = nullptr;
+    unsigned long long *bar = nullptr;
+    MSK_CUDA(cudaMallocAsync((void **)&part, sizeof(double) * (size_t)(3 * nch * R), st));
+    MSK_CUDA(cudaMallocAsync((void **)&bar, sizeof(unsigned long long), st));
+    MSK_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st));
+    CGRArgs A = a;
+    int CHv = CH;
+    void *args[] = {&A, &nb, &CHv, &part, &bar};
+    MSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(NT), args, smem, st));
+    if (launches) *launches += 1;
+    MSK_CUDA(cudaFreeAsync(part, st));
+    MSK_CUDA(cudaFreeAsync(bar, st));
 }
 
 namespace {

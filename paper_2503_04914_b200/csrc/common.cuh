@@ -119,6 +119,34 @@ __device__ __forceinline__ double block_sum(double v, double *smem /* >= NT/32 +
     return smem[NT / 32];
 }
 
+// R independent block sums with block_sum's tree per value (bit-identical to R
+// block_sum calls); smem >= R * (NT/32 + 1).  Results returned in v.
+template <int NT, int R>
+__device__ __forceinline__ void block_sum_r(double (&v)[R], double *smem) {
+    constexpr int W = NT / 32 + 1;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        for (int o = 16; o > 0; o >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) smem[r * W + w] = v[r];
+    }
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double t = lane < NT / 32 ? smem[r * W + lane] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) smem[r * W + NT / 32] = t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = smem[r * W + NT / 32];
+}
+
 template <int NT>
 __device__ __forceinline__ long long block_sum_ll(long long v, long long *smem) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -117,6 +117,87 @@ __global__ void __launch_bounds__(NT, MSK_GMINB) k_gather(GatherArgs a) {
     }
 }
 
+template <int D, int K, int R>
+__global__ void __launch_bounds__(NT, 3) k_gather_m(GatherMArgs a) {
+    __shared__ long long sm[NT / 32 + 1];
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    long long hits = 0;
+    if (i < a.nt) {
+        double x[3];
+        float xf[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            x[t] = a.tx[t][i];
+            xf[t] = (float)(x[t] - a.lev[0].g.lo[t]);
+        }
+        double acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = 0.0;
+        int hl[HMAX];
+        for (int l = 0; l < a.nlev; ++l) {
+            const LevelView &L = a.lev[l];
+            const double d2 = L.delta2, inv = L.inv_delta;
+            const double4 *__restrict__ rec = L.rec;
+            const float4 *__restrict__ frec = L.frec;
+            const double *__restrict__ cf = a.coef[l];
+            const int64_t ldc = a.ldc;
+            const float fthr = L.fthr;
+            double s[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) s[r] = 0.0;
+            int nh = 0;
+            auto flush = [&]() {
+                for (int h = 0; h < nh; ++h) {
+                    const int j = hl[h];
+                    const double4 Q = rec[j];
+                    const double r2 = rec_dist2<D>(x, Q);
+                    if (r2 < d2) {
+                        const double w = wendland<K>(sqrt(r2) * inv);
+#pragma unroll
+                        for (int r = 0; r < R; ++r) s[r] = fma(w, cf[(int64_t)j * ldc + r], s[r]);
+                        ++hits;
+                    }
+                }
+                nh = 0;
+            };
+            for_each_range<D>(L, x, [&](int b, int e) {
+                int j = b;
+                for (; j + 1 < e; j += 2) {
+                    const float4 F0 = frec[j], F1 = frec[j + 1];
+                    float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    float a1 = xf[0] - F1.x, b1 = xf[1] - F1.y, c1 = xf[2] - F1.z;
+                    const bool h0 = fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr;
+                    const bool h1 = fmaf(c1, c1, fmaf(b1, b1, a1 * a1)) < fthr;
+                    if (nh + 2 > HMAX) flush();
+                    if (h0) hl[nh++] = j;
+                    if (h1) hl[nh++] = j + 1;
+                }
+                if (j < e) {
+                    const float4 F0 = frec[j];
+                    float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    if (nh + 1 > HMAX) flush();
+                    if (fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr) hl[nh++] = j;
+                }
+            });
+            flush();
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = fma(L.scale, s[r], acc[r]);
+        }
+        const int64_t bi = a.base_perm ? a.base_perm[i] : i;
+        const int64_t oi = a.out_perm ? a.out_perm[i] : i;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double v = a.sign * acc[r];
+            if (a.base) v = (r < a.bcols ? a.base[bi * a.ldb + a.bcol0 + r] : 0.0) + v;
+            if (r < a.wcols) a.out[oi * a.ldo + a.ocol0 + r] = v;
+        }
+    }
+    if (a.hits) {
+        long long tot = block_sum_ll<NT>(hits, sm);
+        if (threadIdx.x == 0) atomicAdd(a.hits, (unsigned long long)tot);
+    }
+}
+
 __global__ void k_pack(int64_t n, int d, const double *__restrict__ x0, const double *__restrict__ x1,
                        const double *__restrict__ x2, const double *__restrict__ c,
                        double4 *__restrict__ rec) {
@@ -169,6 +250,23 @@ void gather(const GatherArgs &a, cudaStream_t st, int *launches) {
         if (a.k == 0) MSK_G(3, 0); else if (a.k == 1) MSK_G(3, 1); else MSK_G(3, 2);
     }
 #undef MSK_G
+    MSK_CHECK_LAUNCH();
+    if (launches) *launches += 1;
+}
+
+void gather_multi(const GatherMArgs &a, cudaStream_t st, int *launches) {
+    if (a.nt == 0) return;
+    unsigned nb = ceil_div_u(a.nt, NT);
+    if (a.R != 2 && a.R != 4) throw Error(1, "gather_multi: R must be 2 or 4");
+#define MSK_GM(DD, KK, RR) k_gather_m<DD, KK, RR><<<nb, NT, 0, st>>>(a)
+#define MSK_GMK(DD, RR)                                                                  \
+    do {                                                                               \
+        if (a.k == 0) MSK_GM(DD, 0, RR); else if (a.k == 1) MSK_GM(DD, 1, RR); else MSK_GM(DD, 2, RR); \
+    } while (0)
+    if (a.d == 2) { if (a.R == 2) MSK_GMK(2, 2); else MSK_GMK(2, 4); }
+    else { if (a.R == 2) MSK_GMK(3, 2); else MSK_GMK(3, 4); }
+#undef MSK_GMK
+#undef MSK_GM
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
 }

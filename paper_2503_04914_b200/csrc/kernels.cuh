@@ -54,6 +54,29 @@ struct GatherArgs {
     unsigned long long *hits;
 };
 void gather(const GatherArgs &a, cudaStream_t st, int *launches);
+// multi-RHS kernel sums (msk_solve_multi / msk_evaluate_multi): R coefficient
+// columns per source level (spatial rows, row stride ldc); per column the same
+// arithmetic, in the same order, as gather() -- bit-identical to R single runs.
+struct GatherMArgs {
+    int d, k, R;
+    int64_t nt;
+    const double *tx[3];
+    int nlev;
+    LevelView lev[kMaxLevels];   // cells, .rec (coordinates), .frec
+    const double *coef[kMaxLevels];
+    int64_t ldc;
+    const double *base;          // optional: base[(perm ? perm[i] : i) * ldb + bcol0 + r], r < bcols
+    const int32_t *base_perm;
+    int64_t ldb;
+    int bcol0, bcols;
+    double sign;
+    double *out;                 // out[(perm ? perm[i] : i) * ldo + ocol0 + r], r < wcols
+    const int32_t *out_perm;
+    int64_t ldo;
+    int ocol0, wcols;
+    unsigned long long *hits;
+};
+void gather_multi(const GatherMArgs &a, cudaStream_t st, int *launches);
 // rec[i] = (x, y, z, coef) (2-D: (x, y, coef, 0)) from SoA xs (d arrays of n)
 void pack_records(int64_t n, int d, const double *xs, const double *coef, double4 *rec,
                   cudaStream_t st, int *launches);
@@ -89,6 +112,33 @@ struct CGLevelArgs {
     double *coef;             // optional: CG scalars (alpha_k, beta_k) of iterations k < coef_cap
     int coef_cap;             //   (Lanczos tridiagonal -> kappa estimate, msk_solve_info.kappa_est)
 };
+// ---- multi-RHS CG (msk_solve_multi; cg.cu): one level, R right-hand sides
+// with their own scalars; per column the arithmetic of k_cg (bit-identical to
+// R single solves).  Vectors are [n][R] row-major in spatial order.
+struct CGRArgs {
+    int64_t n, nnz;
+    const int64_t *row_ptr;
+    const int32_t *col;
+    const double *val;
+    const double *b;             // spatial [n][R], or null: b_src (caller order) below
+    const double *b_src;         // b_src[b_perm[i] * ldb + col0 + r], r < nvalid (else 0)
+    const int32_t *b_perm;
+    int64_t ldb;
+    int col0, nvalid;
+    double *x;                   // spatial, row stride ldx
+    int64_t ldx;
+    double *r, *p, *q;           // spatial [n][R]
+    double *x_out;               // optional: x_out[x_perm[i] * ldo + col0 + r] = x[i][r], r < nvalid
+    const int32_t *x_perm;
+    int64_t ldo;
+    double tol2;
+    int max_iter;
+    int *out_iters;              // R
+    double *out_rr;              // 2R: final rr, bb per column
+    int *out_status;             // R
+};
+void cg_multi(const CGRArgs &a, int R, cudaStream_t st, int *launches);
+
 // ---- distributed CG (partitioned levels; cg.cu)
 constexpr int kMaxParts = 16;
 struct DistCGScalars {
