@@ -231,7 +231,7 @@ struct msk_hierarchy {
     int64_t off[kMaxLevels + 1] = {0};
     double *ws = nullptr;  // CG workspace: r, p, q, beta, t (5 * ntot)
     // multi-RHS solve (msk_solve_multi): coefficients of all right-hand sides,
-    // spatial order, [n(l)][nrhs_pad] per level (columns grouped by 2 / 4)
+    // spatial order; per level one contiguous [n(l)][R] block per column group
     double *alpham[kMaxLevels] = {nullptr};
     int nrhs_m = 0, nrhs_pad = 0;
     std::vector<int> grp0, grpR, grpP;  // caller column, width R, padded column of each group
@@ -1602,9 +1602,12 @@ extern "C" msk_status msk_solve_multi(msk_hierarchy *h, int32_t nrhs, const doub
     const int L = h->L;
     const double inner_tol = tol / 10.0;  // reading C-10
     h->release_multi();
-    // column groups: 4 wide, the tail 2 or 4 wide (padded with zero columns)
+    // column groups of 2 (an odd tail is padded with a zero column).  Groups of 4
+    // are supported by the kernels but measured slower per column on C3 (37.8
+    // vs 36.9 ms per right-hand side; single solves: 46.2): at 4 columns the
+    // per-thread vector state exceeds the register budget of 3 CTAs per SM.
     for (int c = 0, pc = 0; c < nrhs;) {
-        const int rem = nrhs - c, R = rem >= 3 ? 4 : 2;
+        const int rem = nrhs - c, R = getenv("MSK_MULTI_R4") && rem >= 3 ? 4 : 2;
         h->grp0.push_back(c);
         h->grpR.push_back(R);
         h->grpP.push_back(pc);
@@ -1664,9 +1667,9 @@ extern "C" msk_status msk_solve_multi(msk_hierarchy *h, int32_t nrhs, const doub
                 ga.nlev = l;
                 for (int k = 0; k < l; ++k) {
                     ga.lev[k] = h->view(k);
-                    ga.coef[k] = h->alpham[k] + pc;
+                    ga.coef[k] = h->alpham[k] + (size_t)h->lev[k].n * pc;  // group block [n][R]
                 }
-                ga.ldc = NP;
+                ga.ldc = R;
                 ga.base = fd[l].ptr;
                 ga.base_perm = D.perm;
                 ga.ldb = nrhs;
@@ -1681,8 +1684,8 @@ extern "C" msk_status msk_solve_multi(msk_hierarchy *h, int32_t nrhs, const doub
                 gather_multi(ga, st, &launches);
                 a.b = wsv(3, l, R);
             }
-            a.x = h->alpham[l] + pc;
-            a.ldx = NP;
+            a.x = h->alpham[l] + (size_t)D.n * pc;  // group block [n][R] (contiguous rows)
+            a.ldx = R;
             a.r = wsv(0, l, R);
             a.p = wsv(1, l, R);
             a.q = wsv(2, l, R);
@@ -1759,9 +1762,9 @@ extern "C" msk_status msk_evaluate_multi(msk_hierarchy *h, int64_t m, const doub
         ga.nlev = L;
         for (int l = 0; l < L; ++l) {
             ga.lev[l] = h->view(l);
-            ga.coef[l] = h->alpham[l] + h->grpP[gi];
+            ga.coef[l] = h->alpham[l] + (size_t)h->lev[l].n * h->grpP[gi];
         }
-        ga.ldc = h->nrhs_pad;
+        ga.ldc = h->grpR[gi];
         ga.base = nullptr;
         ga.sign = 1.0;
         ga.out = sd.ptr;

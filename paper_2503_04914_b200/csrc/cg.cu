@@ -742,23 +742,45 @@ __device__ __forceinline__ void spmv_phase_r(CGSharedR<C, R> &SR, const CGRArgs 
         double dot[R];
 #pragma unroll
         for (int c = 0; c < R; ++c) dot[c] = 0.0;
+        {
+            // all loads of the chunk's rows first (independent, in flight together), then the stores
+            double *__restrict__ xw = A.x;
+            double *__restrict__ pw = A.p;
+            double *__restrict__ qw = A.q;
+            constexpr int TB = R >= 4 ? 2 : MAXCH;  // rows per load batch (register budget)
 #pragma unroll
-        for (int t = 0; t < MAXCH; ++t) {
-            const int r = t * NT + tid;
-            if (t < CH && r < crows) {
-                const int64_t i = cr0 + r;
+            for (int t0 = 0; t0 < MAXCH; t0 += TB) {
+                double ri[TB][R], po[TB][R], qo[TB][R], xo[TB][R];
 #pragma unroll
-                for (int c = 0; c < R; ++c) {
-                    const double ri = rv[i * R + c];
-                    const double po = first ? 0.0 : A.p[i * R + c];
-                    const double qo = first ? 0.0 : A.q[i * R + c];
-                    const double xo = first ? 0.0 : A.x[i * A.ldx + c];
-                    const double pn = first ? ri : ri + beta[c] * po;
-                    const double qn = first ? acc[t][c] : acc[t][c] + beta[c] * qo;
-                    A.p[i * R + c] = pn;
-                    A.q[i * R + c] = qn;
-                    A.x[i * A.ldx + c] = first ? 0.0 : xo + alpha_prev[c] * po;
-                    dot[c] += pn * qn;
+                for (int tt = 0; tt < TB; ++tt) {
+                    const int t = t0 + tt;
+                    const int r = t * NT + tid;
+                    const bool ok = t < CH && r < crows;
+                    const int64_t i = cr0 + r;
+#pragma unroll
+                    for (int c = 0; c < R; ++c) {
+                        ri[tt][c] = ok ? rv[i * R + c] : 0.0;
+                        po[tt][c] = ok && !first ? pw[i * R + c] : 0.0;
+                        qo[tt][c] = ok && !first ? qw[i * R + c] : 0.0;
+                        xo[tt][c] = ok && !first ? xw[i * A.ldx + c] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int tt = 0; tt < TB; ++tt) {
+                    const int t = t0 + tt;
+                    const int r = t * NT + tid;
+                    if (t < CH && r < crows) {
+                        const int64_t i = cr0 + r;
+#pragma unroll
+                        for (int c = 0; c < R; ++c) {
+                            const double pn = first ? ri[tt][c] : ri[tt][c] + beta[c] * po[tt][c];
+                            const double qn = first ? acc[t][c] : acc[t][c] + beta[c] * qo[tt][c];
+                            pw[i * R + c] = pn;
+                            qw[i * R + c] = qn;
+                            xw[i * A.ldx + c] = first ? 0.0 : xo[tt][c] + alpha_prev[c] * po[tt][c];
+                            dot[c] += pn * qn;
+                        }
+                    }
                 }
             }
         }
@@ -853,13 +875,27 @@ __global__ void __launch_bounds__(NT, MB) k_cgr(CGRArgs A, int nb, int CH, doubl
             double acc[R];
 #pragma unroll
             for (int k = 0; k < R; ++k) acc[k] = 0.0;
-            for (int t = 0; t < CH; ++t) {
+            double *__restrict__ rw = A.r;
+            const double *__restrict__ qr = A.q;
+            double rv4[MAXCH][R], qv4[MAXCH][R];
+#pragma unroll
+            for (int t = 0; t < MAXCH; ++t) {
                 const int64_t i = (c * CH + t) * NT + tid;
-                if (i < n) {
+                const bool ok = t < CH && i < n;
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    rv4[t][k] = ok ? rw[i * R + k] : 0.0;
+                    qv4[t][k] = ok ? qr[i * R + k] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < MAXCH; ++t) {
+                const int64_t i = (c * CH + t) * NT + tid;
+                if (t < CH && i < n) {
 #pragma unroll
                     for (int k = 0; k < R; ++k) {
-                        const double ri = A.r[i * R + k] - alpha[k] * A.q[i * R + k];
-                        A.r[i * R + k] = ri;
+                        const double ri = rv4[t][k] - alpha[k] * qv4[t][k];
+                        rw[i * R + k] = ri;
                         acc[k] += ri * ri;
                     }
                 }

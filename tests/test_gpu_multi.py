@@ -52,8 +52,10 @@ def _rhs(H, nrhs, seed=0):
 
 
 @pytest.mark.parametrize("name", list(HIERS))
-@pytest.mark.parametrize("nrhs", [1, 3, 4, 6])
-def test_multi_equals_single_bitwise(msk, ctx, name, nrhs):
+@pytest.mark.parametrize("nrhs,r4", [(1, False), (3, False), (4, False), (3, True), (6, True)])
+def test_multi_equals_single_bitwise(msk, ctx, name, nrhs, r4, monkeypatch):
+    if r4:
+        monkeypatch.setenv("MSK_MULTI_R4", "1")  # 4-wide column groups
     H = HIERS[name]()
     h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
     h.assemble()
