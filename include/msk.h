@@ -232,6 +232,18 @@ MSK_API msk_status msk_evaluate(msk_hierarchy *h, int64_t m, const double *x, do
 MSK_API msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x, double *s,
                            msk_eval_info *info);
 
+/* ----------------------------------- truncation diagnostics (§8(f) NEXT-2) */
+
+/* ||M_L||_2 (Figure 1; M = id - T'_L, lower blocks -X_kl =
+ * -B_kl A_l^{-1}, reading C-7) by power iteration on M^T M with M and M^T
+ * applied matrix-free (A_l^{-1}: CG at cg_tol; B_kl, B_kl^T: kernel sums).
+ * Stops when the estimate changes by <= rel_tol relative, or after max_iter
+ * iterations (*iters reports the count; nullable).  The estimate increases
+ * towards ||M||_2 from below.  Requires msk_assemble (assembled A_l, one GPU);
+ * L = 1 gives 0. */
+MSK_API msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_tol, double cg_tol, double *norm,
+                      int32_t *iters);
+
 /* ------------------------------------------- multi-RHS */
 
 /* Solve the multiscale system (eq:mas P:284-290, PRUNED schedule as msk_solve)

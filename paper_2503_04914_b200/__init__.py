@@ -124,6 +124,14 @@ def msk_evaluate_multi(h, m, x, s):
     check(load().msk_evaluate_multi(h, int(m), _ptr(x), _ptr(s)))
 
 
+def msk_m_norm(h, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
+    """||M_L||_2 by power iteration (returns (norm, iterations))."""
+    nrm = ctypes.c_double(0.0)
+    it = ctypes.c_int32(0)
+    check(load().msk_m_norm(h, int(max_iter), float(rel_tol), float(cg_tol), ctypes.byref(nrm), ctypes.byref(it)))
+    return nrm.value, it.value
+
+
 def msk_evaluate(h, m, x, s):
     check(load().msk_evaluate(h, int(m), _ptr(x), _ptr(s)))
 
@@ -299,6 +307,10 @@ class Hierarchy:
         t = msk_solve_multi(self.handle, nrhs, F, tol, max_iter, alpha, iters)
         self.nrhs = nrhs
         return alpha, iters.reshape(self.L, nrhs), t
+
+    def m_norm(self, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
+        """||M_L||_2 (Figure 1) by power iteration on the GPU: (norm, iterations)."""
+        return msk_m_norm(self.handle, max_iter, rel_tol, cg_tol)
 
     def evaluate_multi(self, x):
         x = _f64(x)

@@ -1780,6 +1780,109 @@ extern "C" msk_status msk_evaluate_multi(msk_hierarchy *h, int64_t m, const doub
     API_END
 }
 
+// ================================================= truncation diagnostics
+// NEXT-2: ||M_L||_2 (Figure 1) by power iteration
+// on M^T M with M applied matrix-free: M v = -(B A^{-1}) v blockwise (the
+// lower blocks -X_kl = -B_kl A_l^{-1}, reading C-7), M^T u = -A^{-1} (B^T u)
+// blockwise; the A_l^{-1} are CG solves (one batched launch per application),
+// B and B^T kernel sums (gather / gather_t).  sigma = ||M v|| with ||v|| = 1.
+namespace {
+__global__ void k_start_vector(double *v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i < n) v[i] = (double)(((uint64_t)(i + 1) * 2654435761ull) & 0xffffffffull) * 0x1p-32 - 0.5;
+}
+}  // namespace
+
+extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_tol, double cg_tol,
+                                 double *norm, int32_t *iters) {
+    API_BEGIN
+    require(h && norm, "msk_m_norm: NULL argument");
+    require(max_iter >= 1 && rel_tol > 0.0 && cg_tol > 0.0 && cg_tol < 1.0, "msk_m_norm: bad arguments");
+    if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_m_norm: call msk_assemble first");
+    require(!(h->flags & MSK_FLAG_MATRIX_FREE) && h->ctx->world == 1,
+            "msk_m_norm: needs assembled A_l on one GPU");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    cudaStream_t st = h->st();
+    const int L = h->L;
+    const int64_t N = h->ntot;
+    *norm = 0.0;
+    if (iters) *iters = 0;
+    if (L < 2) return MSK_OK;
+    h->ensure_ws();
+    double *v = dalloc<double>((size_t)N, st), *u = dalloc<double>((size_t)N, st);
+    double *w = dalloc<double>((size_t)N, st), *t = dalloc<double>((size_t)N, st);
+    double *scratch = dalloc<double>(300, st);
+    int *d_it = dalloc<int>((size_t)L, st), *d_stat = dalloc<int>((size_t)L, st);
+    double *d_rr = dalloc<double>((size_t)(2 * L), st);
+    k_start_vector<<<ceil_div_u(N, 256), 256, 0, st>>>(v, N);
+    MSK_CHECK_LAUNCH();
+    dev_scale(v, 1.0 / sqrt(dev_dot(v, v, N, scratch, st)), N, st);
+    // A_l^{-1} for l < L-1 on all those levels in one launch: x_l = A_l^{-1} b_l
+    auto solve_coarse = [&](const double *b, double *x) {
+        std::vector<CGLevelArgs> a;
+        for (int l = 0; l + 1 < L; ++l)
+            a.push_back(cg_args(h, l, cg_tol, 20000, b + h->off[l], nullptr, x + h->off[l], nullptr, d_it + l,
+                                d_rr + 2 * l, d_stat + l));
+        cg_batched(a.data(), (int)a.size(), st, nullptr);
+    };
+    double sigma = 0.0;
+    int it = 0;
+    for (; it < max_iter; ++it) {
+        // u = M v
+        solve_coarse(v, t);
+        MSK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * (size_t)h->lev[0].n, st));
+        for (int l = 0; l + 1 < L; ++l) h->pack(l, t + h->off[l], nullptr);
+        for (int k = 1; k < L; ++k) {
+            GatherArgs ga{};
+            ga.d = h->d;
+            ga.k = h->k;
+            ga.nt = h->lev[k].n;
+            for (int a = 0; a < h->d; ++a) ga.tx[a] = h->lev[k].xs + (size_t)a * h->lev[k].n;
+            ga.nlev = k;
+            for (int l = 0; l < k; ++l) ga.lev[l] = h->view(l, t + h->off[l]);
+            ga.sign = -1.0;
+            ga.out = u + h->off[k];
+            gather(ga, st, nullptr);
+        }
+        const double s_new = sqrt(dev_dot(u, u, N, scratch, st));
+        // w = M^T u = -A^{-1} (B^T u) on the coarse levels, 0 on the finest
+        for (int l = 0; l + 1 < L; ++l) {
+            GatherTArgs gt{};
+            gt.d = h->d;
+            gt.k = h->k;
+            gt.nt = h->lev[l].n;
+            for (int a = 0; a < h->d; ++a) gt.tx[a] = h->lev[l].xs + (size_t)a * h->lev[l].n;
+            const double dl = h->lev[l].delta;
+            gt.delta2 = dl * dl;
+            gt.inv_delta = 1.0 / dl;
+            gt.scale = -pow(dl, -(double)h->d);  // the minus sign of M^T
+            gt.nsrc = 0;
+            for (int k = l + 1; k < L; ++k) {
+                gt.src[gt.nsrc] = h->view(k);
+                gt.y[gt.nsrc] = u + h->off[k];
+                gt.reach[gt.nsrc] = (int)std::min(floor(dl * h->lev[k].g.inv_cell) + 1.0, 1e6);
+                ++gt.nsrc;
+            }
+            gt.out = t + h->off[l];
+            gather_t(gt, st, nullptr);
+        }
+        solve_coarse(t, w);
+        MSK_CUDA(cudaMemsetAsync(w + h->off[L - 1], 0, sizeof(double) * (size_t)h->lev[L - 1].n, st));
+        const double wn = sqrt(dev_dot(w, w, N, scratch, st));
+        const bool done = it > 0 && fabs(s_new - sigma) <= rel_tol * s_new;
+        sigma = s_new;
+        if (done || !(wn > 0.0)) { ++it; break; }
+        MSK_CUDA(cudaMemcpyAsync(v, w, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, st));
+        dev_scale(v, 1.0 / wn, N, st);
+    }
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(v, st); dfree(u, st); dfree(w, st); dfree(t, st); dfree(scratch, st);
+    dfree(d_it, st); dfree(d_stat, st); dfree(d_rr, st);
+    *norm = sigma;
+    if (iters) *iters = it;
+    API_END
+}
+
 extern "C" msk_status msk_evaluate(msk_hierarchy *h, int64_t m, const double *x, double *s) {
     return msk_evaluate_ex(h, m, x, s, nullptr);
 }

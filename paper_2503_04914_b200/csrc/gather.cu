@@ -198,6 +198,55 @@ __global__ void __launch_bounds__(NT, 3) k_gather_m(GatherMArgs a) {
     }
 }
 
+template <int D, int K>
+__global__ void __launch_bounds__(NT) k_gather_t(GatherTArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (i >= a.nt) return;
+    double x[3];
+#pragma unroll
+    for (int t = 0; t < D; ++t) x[t] = a.tx[t][i];
+    double acc = 0.0;
+    for (int s = 0; s < a.nsrc; ++s) {
+        const LevelView &L = a.src[s];
+        const double *__restrict__ y = a.y[s];
+        double sum = 0.0;
+        for_each_range_m<D>(L, x, a.reach[s], [&](int b, int e) {
+            for (int j = b; j < e; ++j) {
+                double z[3];
+#pragma unroll
+                for (int t = 0; t < D; ++t) z[t] = L.x[t][j];
+                const double r2 = dist2_nofma<D>(x, z);
+                if (r2 < a.delta2) sum = fma(wendland<K>(sqrt(r2) * a.inv_delta), y[j], sum);
+            }
+        });
+        acc = fma(a.scale, sum, acc);
+    }
+    a.out[i] = acc;
+}
+
+__global__ void k_dot_partial(const double *__restrict__ a, const double *__restrict__ b, int64_t n,
+                              double *__restrict__ part) {
+    __shared__ double red[NT / 32 + 2];
+    double t = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT)
+        t = fma(a[i], b[i], t);
+    t = block_sum<NT>(t, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void k_sum_partials(const double *__restrict__ part, int np, double *__restrict__ out) {
+    __shared__ double red[NT / 32 + 2];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < np; i += NT) t += part[i];
+    t = block_sum<NT>(t, red);
+    if (threadIdx.x == 0) *out = t;
+}
+
+__global__ void k_scale(double *v, double s, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (i < n) v[i] *= s;
+}
+
 __global__ void k_pack(int64_t n, int d, const double *__restrict__ x0, const double *__restrict__ x1,
                        const double *__restrict__ x2, const double *__restrict__ c,
                        double4 *__restrict__ rec) {
@@ -269,6 +318,39 @@ void gather_multi(const GatherMArgs &a, cudaStream_t st, int *launches) {
 #undef MSK_GM
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
+}
+
+void gather_t(const GatherTArgs &a, cudaStream_t st, int *launches) {
+    if (a.nt == 0 || a.nsrc == 0) return;
+    unsigned nb = ceil_div_u(a.nt, NT);
+#define MSK_GT(DD, KK) k_gather_t<DD, KK><<<nb, NT, 0, st>>>(a)
+    if (a.d == 2) {
+        if (a.k == 0) MSK_GT(2, 0); else if (a.k == 1) MSK_GT(2, 1); else MSK_GT(2, 2);
+    } else {
+        if (a.k == 0) MSK_GT(3, 0); else if (a.k == 1) MSK_GT(3, 1); else MSK_GT(3, 2);
+    }
+#undef MSK_GT
+    MSK_CHECK_LAUNCH();
+    if (launches) *launches += 1;
+}
+
+// scratch: >= 297 doubles
+double dev_dot(const double *a, const double *b, int64_t n, double *scratch, cudaStream_t st) {
+    constexpr int NB = 296;  // fixed grid: a fixed summation tree
+    k_dot_partial<<<NB, NT, 0, st>>>(a, b, n, scratch);
+    MSK_CHECK_LAUNCH();
+    k_sum_partials<<<1, NT, 0, st>>>(scratch, NB, scratch + NB);
+    MSK_CHECK_LAUNCH();
+    double s = 0.0;
+    MSK_CUDA(cudaMemcpyAsync(&s, scratch + NB, sizeof s, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    return s;
+}
+
+void dev_scale(double *v, double s, int64_t n, cudaStream_t st) {
+    if (n == 0) return;
+    k_scale<<<ceil_div_u(n, NT), NT, 0, st>>>(v, s, n);
+    MSK_CHECK_LAUNCH();
 }
 
 void pack_records(int64_t n, int d, const double *xs, const double *coef, double4 *rec,

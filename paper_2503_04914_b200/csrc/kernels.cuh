@@ -77,6 +77,25 @@ struct GatherMArgs {
     unsigned long long *hits;
 };
 void gather_multi(const GatherMArgs &a, cudaStream_t st, int *launches);
+// transposed B products (msk_m_norm): for target points x_i of level l,
+// out_i = sum_{k in srcs} sum_{j: r < delta_l} delta_l^-d phi(r / delta_l) y_k[j]
+// = sum_k (B_kl^T y_k)_i, the sources enumerated in level k's grid with a reach
+// of `reach[k]` cells (delta_l spans several cells of a finer level).
+struct GatherTArgs {
+    int d, k;
+    int64_t nt;
+    const double *tx[3];
+    double delta2, inv_delta, scale;   // of the TARGET level l (column level of B_kl)
+    int nsrc;
+    LevelView src[kMaxLevels];         // SoA coordinates + cells of level k
+    const double *y[kMaxLevels];       // spatial order
+    int reach[kMaxLevels];
+    double *out;                       // spatial order of the targets
+};
+void gather_t(const GatherTArgs &a, cudaStream_t st, int *launches);
+// deterministic dot product of n doubles (one block-reduction tree; host result)
+double dev_dot(const double *a, const double *b, int64_t n, double *scratch, cudaStream_t st);
+void dev_scale(double *v, double s, int64_t n, cudaStream_t st);
 // rec[i] = (x, y, z, coef) (2-D: (x, y, coef, 0)) from SoA xs (d arrays of n)
 void pack_records(int64_t n, int d, const double *xs, const double *coef, double4 *rec,
                   cudaStream_t st, int *launches);

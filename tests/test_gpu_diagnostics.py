@@ -1,0 +1,67 @@
+"""Truncation diagnostics on the GPU (msk_m_norm).
+
+||M_L||_2 of Figure 1 by power iteration with M and M^T
+applied matrix-free (CG solves + kernel sums, incl. the transposed B^T
+products).  Pinned to the paper's printed values (tests/golden/, every printed
+digit, L = 2..7) and to the dense oracle (L <= 5, 1e-7 relative).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from workloads import grid_hierarchy, halton_hierarchy
+
+pytestmark = pytest.mark.gpu
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+@pytest.fixture(scope="module")
+def msk():
+    import paper_2503_04914_b200 as m
+    m.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(msk):
+    c = msk.Context(0)
+    yield c
+    c.close()
+
+
+def _printed_eq(v, printed, digits=3):
+    return abs(v - printed) <= 0.5 * 10 ** -digits + 1e-12
+
+
+@pytest.mark.parametrize("L", [2, 3, 4, 5, 6, 7])
+def test_figure1_norm_matches_paper(msk, ctx, L):
+    H = grid_hierarchy(L)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    nrm, it = h.m_norm(max_iter=2000, rel_tol=1e-10)
+    assert _printed_eq(nrm, GOLDEN["figure1"]["numerical"][str(L)]), (L, nrm, it)
+    h.close()
+
+
+@pytest.mark.parametrize("name", ["grid4", "halton2d", "halton3d"])
+def test_m_norm_matches_dense_oracle(msk, ctx, name):
+    from oracle import dense
+    H = {"grid4": lambda: grid_hierarchy(4),
+         "halton2d": lambda: halton_hierarchy("h2", 2, [60, 240, 960], 4.0),
+         "halton3d": lambda: halton_hierarchy("h3", 3, [80, 640, 2000], 1.5)}[name]()
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    nrm, it = h.m_norm(max_iter=3000, rel_tol=1e-12)
+    ref = dense.fig1_norm(H.points, H.delta, H.k)
+    assert abs(nrm / ref - 1) < 1e-7, (name, nrm, ref, it)
+    h.close()
+
+
+def test_m_norm_single_level_is_zero(msk, ctx):
+    H = grid_hierarchy(1)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    assert h.m_norm()[0] == 0.0
+    h.close()
