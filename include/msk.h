@@ -243,6 +243,14 @@ MSK_API msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x,
  * L = 1 gives 0. */
 MSK_API msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_tol, double cg_tol, double *norm,
                       int32_t *iters);
+/* which = 0: ||M_L||_2 (as msk_m_norm); which = 1: ||M_L - M~_L(T)||_2 with the
+ * stored thresholded factor of the last msk_assemble(T > 0) (Figure 2,
+ * M - M~ = -(X - X~), X~ applied from the stored CSR and its
+ * transpose; MSK_ERR_STATE without a factor).  The transposed product sums a
+ * column's entries in the order of an atomic fill: reproducible to rounding,
+ * not bit for bit (a diagnostic, not the solve path). */
+MSK_API msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max_iter, double rel_tol,
+                         double cg_tol, double *norm, int32_t *iters);
 
 /* ------------------------------------------- multi-RHS */
 

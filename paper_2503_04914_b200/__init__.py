@@ -132,6 +132,14 @@ def msk_m_norm(h, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
     return nrm.value, it.value
 
 
+def msk_m_norm_ex(h, which, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
+    nrm = ctypes.c_double(0.0)
+    it = ctypes.c_int32(0)
+    check(load().msk_m_norm_ex(h, int(which), int(max_iter), float(rel_tol), float(cg_tol), ctypes.byref(nrm),
+                               ctypes.byref(it)))
+    return nrm.value, it.value
+
+
 def msk_evaluate(h, m, x, s):
     check(load().msk_evaluate(h, int(m), _ptr(x), _ptr(s)))
 
@@ -311,6 +319,10 @@ class Hierarchy:
     def m_norm(self, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
         """||M_L||_2 (Figure 1) by power iteration on the GPU: (norm, iterations)."""
         return msk_m_norm(self.handle, max_iter, rel_tol, cg_tol)
+
+    def m_diff_norm(self, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
+        """||M_L - M~_L(T)||_2 (Figure 2) with the stored factor: (norm, iterations)."""
+        return msk_m_norm_ex(self.handle, 1, max_iter, rel_tol, cg_tol)
 
     def evaluate_multi(self, x):
         x = _f64(x)

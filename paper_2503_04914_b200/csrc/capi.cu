@@ -1793,10 +1793,13 @@ __global__ void k_start_vector(double *v, int64_t n) {
 }
 }  // namespace
 
-extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_tol, double cg_tol,
-                                 double *norm, int32_t *iters) {
+extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max_iter, double rel_tol,
+                                    double cg_tol, double *norm, int32_t *iters) {
     API_BEGIN
     require(h && norm, "msk_m_norm: NULL argument");
+    require(which == 0 || which == 1, "msk_m_norm: which must be 0 (M) or 1 (M - M~(T))");
+    if (which == 1 && !(h->T > 0.0))
+        throw Error(MSK_ERR_STATE, "msk_m_norm: M - M~(T) needs the thresholded factor (msk_assemble with T > 0)");
     require(max_iter >= 1 && rel_tol > 0.0 && cg_tol > 0.0 && cg_tol < 1.0, "msk_m_norm: bad arguments");
     if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_m_norm: call msk_assemble first");
     require(!(h->flags & MSK_FLAG_MATRIX_FREE) && h->ctx->world == 1,
@@ -1813,6 +1816,20 @@ extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_
     double *w = dalloc<double>((size_t)N, st), *t = dalloc<double>((size_t)N, st);
     double *scratch = dalloc<double>(300, st);
     int *d_it = dalloc<int>((size_t)L, st), *d_stat = dalloc<int>((size_t)L, st);
+    // M - M~(T) = -(X - X~): add X~ v (stored CSR) to M v and X~^T u (its transpose) to M^T u
+    int64_t *cptr = nullptr, *cpos = nullptr;
+    int32_t *crow = nullptr, *ccol = nullptr;
+    double *nv = nullptr;
+    const int64_t ncols = h->off[L - 1];
+    if (which == 1) {
+        cptr = dalloc<int64_t>((size_t)(ncols + 1), st);
+        cpos = dalloc<int64_t>((size_t)h->tnnz + 1, st);
+        crow = dalloc<int32_t>((size_t)h->tnnz + 1, st);
+        ccol = dalloc<int32_t>((size_t)h->tnnz + 1, st);
+        thresh_csc(N - h->off[1], h->off[1], h->tnnz, ncols, h->trow_ptr, h->tcol, cptr, cpos, crow, ccol, st,
+                   nullptr);
+        nv = dalloc<double>((size_t)N, st);
+    }
     double *d_rr = dalloc<double>((size_t)(2 * L), st);
     k_start_vector<<<ceil_div_u(N, 256), 256, 0, st>>>(v, N);
     MSK_CHECK_LAUNCH();
@@ -1844,6 +1861,11 @@ extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_
             ga.out = u + h->off[k];
             gather(ga, st, nullptr);
         }
+        if (which == 1) {  // u += X~ v  (thresh_residual: out = base - sum val * (-v))
+            MSK_CUDA(cudaMemcpyAsync(nv, v, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, st));
+            dev_scale(nv, -1.0, N, st);
+            thresh_residual(h->off[1], N, h->trow_ptr, h->tcol, h->tval, u, nv, u, st, nullptr);
+        }
         const double s_new = sqrt(dev_dot(u, u, N, scratch, st));
         // w = M^T u = -A^{-1} (B^T u) on the coarse levels, 0 on the finest
         for (int l = 0; l + 1 < L; ++l) {
@@ -1868,6 +1890,7 @@ extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_
         }
         solve_coarse(t, w);
         MSK_CUDA(cudaMemsetAsync(w + h->off[L - 1], 0, sizeof(double) * (size_t)h->lev[L - 1].n, st));
+        if (which == 1) csc_spmv_add(ncols, cptr, cpos, crow, h->tval, u, w, st);  // w += X~^T u
         const double wn = sqrt(dev_dot(w, w, N, scratch, st));
         const bool done = it > 0 && fabs(s_new - sigma) <= rel_tol * s_new;
         sigma = s_new;
@@ -1878,9 +1901,15 @@ extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_
     MSK_CUDA(cudaStreamSynchronize(st));
     dfree(v, st); dfree(u, st); dfree(w, st); dfree(t, st); dfree(scratch, st);
     dfree(d_it, st); dfree(d_stat, st); dfree(d_rr, st);
+    dfree(cptr, st); dfree(cpos, st); dfree(crow, st); dfree(ccol, st); dfree(nv, st);
     *norm = sigma;
     if (iters) *iters = it;
     API_END
+}
+
+extern "C" msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_tol, double cg_tol,
+                                 double *norm, int32_t *iters) {
+    return msk_m_norm_ex(h, 0, max_iter, rel_tol, cg_tol, norm, iters);
 }
 
 extern "C" msk_status msk_evaluate(msk_hierarchy *h, int64_t m, const double *x, double *s) {

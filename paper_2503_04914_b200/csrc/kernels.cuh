@@ -248,6 +248,8 @@ struct ThreshValueArgs {
 };
 void thresh_values(const ThreshValueArgs &a, cudaStream_t st, int *launches);
 // out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)
+void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,
+                  const double *u, double *out, cudaStream_t st);
 void thresh_residual(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col, const double *val,
                      const double *base, const double *v, double *out, cudaStream_t st, int *launches);
 

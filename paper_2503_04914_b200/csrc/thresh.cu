@@ -212,7 +212,26 @@ __global__ void __launch_bounds__(NT) k_tresidual(int64_t r0, int64_t r1, const 
     for (int64_t p = row_ptr[g]; p < row_ptr[g + 1]; ++p) s += val[p] * v[col[p]];
     out[g] = base[g] - s;
 }
+// out[c] += sum over column c's entries of val[cpos[k]] * u[crow[k]] (transposed SpMV)
+__global__ void __launch_bounds__(NT) k_csc_spmv_add(int64_t ncols, const int64_t *__restrict__ cptr,
+                                                     const int64_t *__restrict__ cpos,
+                                                     const int32_t *__restrict__ crow,
+                                                     const double *__restrict__ val, const double *__restrict__ u,
+                                                     double *__restrict__ out) {
+    const int64_t c = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (c >= ncols) return;
+    double s = 0.0;
+    for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k) s = fma(val[cpos[k]], u[crow[k]], s);
+    out[c] += s;
+}
 }  // namespace
+
+void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,
+                  const double *u, double *out, cudaStream_t st) {
+    if (ncols <= 0) return;
+    k_csc_spmv_add<<<ceil_div_u(ncols, NT), NT, 0, st>>>(ncols, cptr, cpos, crow, val, u, out);
+    MSK_CHECK_LAUNCH();
+}
 
 void thresh_count(const ThreshPatternArgs &a, cudaStream_t st, int *launches) {
     if (a.nt == 0) return;

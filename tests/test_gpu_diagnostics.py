@@ -65,3 +65,23 @@ def test_m_norm_single_level_is_zero(msk, ctx):
     h.assemble()
     assert h.m_norm()[0] == 0.0
     h.close()
+
+
+@pytest.mark.parametrize("L", [3, 4, 5, 6, 7])
+def test_figure2_ratio_matches_paper(msk, ctx, L):
+    """||M_L - M~_L(T)||_2 / ||M_L||_2, T = 1..6 (PAPER.md:1365-1413): every
+    printed digit, with the stored thresholded factor (a6) and its transpose;
+    L = 7 is beyond the dense oracle."""
+    H = grid_hierarchy(L)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    m, _ = h.m_norm(max_iter=2000, rel_tol=1e-11)
+    got = []
+    for T in range(1, 7):
+        h.assemble(T=float(T), lagrange_tol=1e-14)
+        d, it = h.m_diff_norm(max_iter=3000, rel_tol=1e-11)
+        got.append(d / m)
+    want = GOLDEN["figure2"][str(L)]
+    for T, (g, w) in enumerate(zip(got, want), start=1):
+        assert _printed_eq(g, w, 5), (L, T, g, w)
+    h.close()
