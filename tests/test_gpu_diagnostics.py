@@ -85,3 +85,22 @@ def test_figure2_ratio_matches_paper(msk, ctx, L):
     for T, (g, w) in enumerate(zip(got, want), start=1):
         assert _printed_eq(g, w, 5), (L, T, g, w)
     h.close()
+
+
+@pytest.mark.parametrize("L", [3, 4, 5, 6])
+def test_figure3_nnz_ratio_matches_paper(msk, ctx, L):
+    """nnz(M~_L(T)) / nnz(M_L), T = 1..6, entries counted
+    as |v| > 1e-8 (reading C-6) from the stored factor; T = 1e9 keeps every
+    entry of X (the denominator)."""
+    def count(h):
+        return sum(int(np.count_nonzero(np.abs(h.export_factor(k, l)[2]) > 1e-8))
+                   for k in range(1, L) for l in range(k))
+    H = grid_hierarchy(L)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble(T=1e9, lagrange_tol=1e-14)
+    den = count(h)
+    want = GOLDEN["figure3"][str(L)]
+    for T in range(1, 7):
+        h.assemble(T=float(T), lagrange_tol=1e-14)
+        assert _printed_eq(count(h) / den, want[T - 1], 5), (L, T)
+    h.close()
