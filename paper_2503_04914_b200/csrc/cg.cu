@@ -331,7 +331,8 @@ __device__ __forceinline__ void issue_piece_t(SH &S, int b, const int32_t *col, 
 // Chunks handled: cbase + me + k*nb for k = 0.. while < cbase + nloc (cbase =
 // 0, nloc = all chunks on one GPU; the owned chunk range of a partition in
 // the distributed CG).  L.row_ptr is indexed by global row.
-template <int C>
+// PLAIN: y = A v only (msk_apply_block): v = L.r, y = L.q, no updates, no dot.
+template <int C, bool PLAIN = false>
 __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
                                            int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol,
                                            bool first, double alpha_prev, double beta) {
@@ -369,7 +370,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
         const uint32_t cs = ps.CS + (uint32_t)k;
         // the epilogue's own-row vectors of the NEXT chunk -> L2 (hidden behind
         // this chunk's pieces; 33.38 -> 33.1 ms on the C3 finest level)
-        if (tid == 0 && !first && k + 1 < K) {
+        if (!PLAIN && tid == 0 && !first && k + 1 < K) {
             int64_t nr0;
             int nrows;
             chunk_rows(k + 1, nr0, nrows);
@@ -440,7 +441,13 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             kb = ke;
         }
         double dot = 0.0;
-        {
+        if (PLAIN) {
+#pragma unroll
+            for (int t = 0; t < MAXCH; ++t) {
+                const int r = t * NT + tid;
+                if (t < CH && r < crows) L.q[cr0 + r] = acc[t];
+            }
+        } else {
             double *__restrict__ x = L.x;
             double *__restrict__ p = L.p;
             double *__restrict__ q = L.q;
@@ -471,7 +478,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
         }
         const double s = block_sum<NT>(dot, S.red);  // its barriers also retire rp buffer cs&1
         if (tid == 0) {
-            part_out[cbase + me + k * nb] = s;
+            if (!PLAIN) part_out[cbase + me + k * nb] = s;
             if (k + 2 < K) {
                 int64_t nr0;
                 int nrows;
@@ -942,7 +949,26 @@ __global__ void __launch_bounds__(NT, MB) k_cgr(CGRArgs A, int nb, int CH, doubl
     }
 }
 
-// standalone y = A v (msk_apply_block): one CTA per tile
+// standalone y = A v (msk_apply_block): the CG's pipelined SpMV pass without
+// the CG epilogue, persistent grid (one CTA per resident slot, chunks round robin)
+template <int C, int MB>
+__global__ void __launch_bounds__(NT, MB) k_spmv_t(CGLevelArgs L, int CH) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CGSharedTT<C> &S = *reinterpret_cast<CGSharedTT<C> *>(smem_raw);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        mbar_init(&S.bar_rp[0], 1);
+        mbar_init(&S.bar_rp[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    PipeState ps{0u, 0u};
+    const int64_t nch = ((L.n + NT - 1) / NT + CH - 1) / CH;
+    spmv_phase<C, true>(S, L, blockIdx.x, gridDim.x, 0, nch, CH, nullptr, ps, policy_evict_first(), false, 0.0,
+                        0.0);
+}
+
+// (superseded warp-pipelined standalone SpMV, kept for reference timings)
 __global__ void __launch_bounds__(NT) k_spmv(int64_t n, const int64_t *__restrict__ row_ptr,
                                              const int32_t *__restrict__ col,
                                              const double *__restrict__ val,
@@ -1428,7 +1454,32 @@ void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
               const double *v, double *y, cudaStream_t st, int *launches) {
     if (n == 0) return;
     set_smem_attrs();
-    k_spmv<<<ceil_div_u(n, NT), NT, sizeof(CGShared), st>>>(n, row_ptr, col, val, v, y);
+    static bool attr = false;
+    if (!attr) {
+        MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT0, MINB0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(CGSharedTT<CAPT0>)));
+        MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT1, MINB1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(CGSharedTT<CAPT1>)));
+        attr = true;
+    }
+    CGLevelArgs L{};
+    L.n = n;
+    L.row_ptr = row_ptr;
+    L.col = col;
+    L.val = val;
+    L.r = const_cast<double *>(v);
+    L.q = y;
+    int64_t nnz = 0;
+    MSK_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof nnz, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    const int CH = cg_chunk_tiles(n);
+    const int64_t nch = ((n + NT - 1) / NT + CH - 1) / CH;
+    const int vi = cg_variant((double)nnz, (double)n);  // long rows: 4096-entry pieces
+    const int grid = (int)(nch < g_var[vi].resident ? nch : g_var[vi].resident);
+    if (vi == 1)
+        k_spmv_t<CAPT1, MINB1><<<grid, NT, sizeof(CGSharedTT<CAPT1>), st>>>(L, CH);
+    else
+        k_spmv_t<CAPT0, MINB0><<<grid, NT, sizeof(CGSharedTT<CAPT0>), st>>>(L, CH);
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
 }

@@ -59,6 +59,18 @@ def main():
     out["spmv_ms"] = t
     out["spmv_GBs"] = byts / (t * 1e-3) / 1e9
     out["spmv_GNNZs"] = nnz / (t * 1e-3) / 1e9
+    # matrix-free y = A v of the same level (kernel sum over the cell list)
+    hm = msk.Hierarchy(ctx, [torch.from_numpy(p).to(dev) for p in H.points], H.delta, H.q, k=H.k,
+                       flags=msk.MSK_FLAG_MATRIX_FREE)
+    hm.assemble()
+    ts = []
+    for _ in range(args.reps + 1):
+        _, t = hm.apply_block(lf, lf, v, y)
+        ts.append(t)
+    t = float(np.median(ts[1:]))
+    out["spmv_mf_ms"] = t
+    out["spmv_mf_GNNZs"] = nnz / (t * 1e-3) / 1e9
+    hm.close()
     b = torch.from_numpy(H.f()[lf]).to(dev)
     ts, its = [], []
     for _ in range(2):
