@@ -209,6 +209,19 @@ MSK_API msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_
  * Non-convergence of a Lagrange solve => MSK_ERR_NOCONV. */
 MSK_API msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol);
 
+/* msk_assemble with local-patch Lagrange functions for
+ * the coarse levels with more than patch_min_n points (patch_R > 0): the
+ * coefficients of chi_i^(l) solve A_l restricted to the patch
+ * {x_h : ||x_h - x_i^(l)|| < patch_R q_l} (zero outside; Lagrange functions
+ * decay exponentially away from x_i, Lemma lagrangedecay), one CTA
+ * and one shared-memory system per column, so the build costs O(N(l)) instead
+ * of O(N(l)^2).  An approximation of the exact factor: the error at the stored
+ * entries falls with patch_R - T.  patch_R <= 0: exactly
+ * msk_assemble.  A patch that does not fit in shared memory =>
+ * MSK_ERR_INVALID (reduce patch_R). */
+MSK_API msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrange_tol, double patch_R,
+                           int64_t patch_min_n);
+
 /* a3-a5, a8: solve T_L alpha = f (eq:bigt) through eq:split.
  *   f      L pointers to f^{(l)} (n[l] FP64, caller order, host or device).
  *   tol    relative CG tolerance in (0,1): stop when ||r||_2 <= tol ||b||_2

@@ -103,6 +103,10 @@ def msk_assemble(h, T=0.0, lagrange_tol=1e-13):
     check(load().msk_assemble(h, float(T), float(lagrange_tol)))
 
 
+def msk_assemble_ex(h, T, lagrange_tol, patch_R, patch_min_n):
+    check(load().msk_assemble_ex(h, float(T), float(lagrange_tol), float(patch_R), int(patch_min_n)))
+
+
 def msk_solve(h, f, tol, max_iter, schedule, alpha):
     fp, k1 = _ptr_array(f)
     ap, k2 = _ptr_array(alpha)
@@ -287,8 +291,13 @@ class Hierarchy:
     def info(self) -> HierarchyInfo:
         return msk_hierarchy_info_get(self.handle)
 
-    def assemble(self, T: float = 0.0, lagrange_tol: float = 1e-13):
-        msk_assemble(self.handle, T, lagrange_tol)
+    def assemble(self, T: float = 0.0, lagrange_tol: float = 1e-13, patch_R: float = 0.0, patch_min_n: int = 0):
+        """patch_R > 0: local-patch Lagrange functions of radius patch_R * q_l on the
+        coarse levels with more than patch_min_n points (msk_assemble_ex)."""
+        if patch_R > 0.0:
+            msk_assemble_ex(self.handle, T, lagrange_tol, patch_R, patch_min_n)
+        else:
+            msk_assemble(self.handle, T, lagrange_tol)
 
     def solve(self, f, tol=1e-12, max_iter=20000, schedule="pruned", alpha=None):
         f = [_f64(x) for x in f]

@@ -245,6 +245,7 @@ struct msk_hierarchy {
     int32_t *tcol = nullptr;
     double *tval = nullptr;
     int lagrange_max_iters = 0;
+    int patch_max_points = 0;
     double t_lagrange_ms = 0;
     // distributed solve: per level, the row partition and this process's
     // partitions (one per rank over NCCL, all of them in the emulation)
@@ -607,7 +608,8 @@ namespace {
 // P:846-861): geometric pattern ||x_j^(k) - x_i^(l)||^2 < (T q_l)^2 (reading
 // C-5), values chi_i^(l)(x_j^(k)) from Lagrange columns c_i = A_l^{-1} e_i
 // solved by the multi-RHS CG at lagrange_tol (eq:chi P:373-377).
-void build_factor(msk_hierarchy *h, double T, double lagrange_tol, int *launches) {
+void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_R, int64_t patch_min_n,
+                  int *launches) {
     cudaStream_t st = h->st();
     const int L = h->L, d = h->d;
     const int64_t ntot = h->ntot;
@@ -661,12 +663,61 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, int *launches
     MSK_CUDA(cudaMemcpyAsync(hcptr.data(), cptr, sizeof(int64_t) * (ncols + 1), cudaMemcpyDeviceToHost, st));
     int *dstat = dalloc<int>(2, st);
     MSK_CUDA(cudaMemsetAsync(dstat, 0, 2 * sizeof(int), st));
+    int *pstat = dalloc<int>(5, st);  // patch path: CG failures, overflows, max iterations, max patch, count
+    MSK_CUDA(cudaMemsetAsync(pstat, 0, 5 * sizeof(int), st));
     MSK_CUDA(cudaStreamSynchronize(st));
     // ---- Lagrange columns, level by level, rounds of concurrent 32-column batches
     const int resident = 4 * 148;
     const double budget = 8e9;  // bytes of CG workspace per round
     for (int l = 0; l + 1 < L; ++l) {
         const LevelData &D = h->lev[l];
+        if (patch_R > 0.0 && D.n > patch_min_n) {
+            // ---- local-patch Lagrange functions, one CTA per column
+            PatchArgs pa{};
+            pa.d = d;
+            pa.k = h->k;
+            pa.L = L;
+            pa.ncols = D.n;
+            const double rho = patch_R * D.q;
+            pa.rho2 = rho * rho;
+            pa.reach = (int)std::min(floor(rho * D.g.inv_cell) + 1.0, 1e6);
+            pa.Lv = h->view(l);
+            pa.row_ptr = D.row_ptr;
+            pa.col = D.col;
+            pa.val = D.val;
+            pa.tol2 = lagrange_tol * lagrange_tol;
+            pa.max_iter = 5000;
+            pa.cptr = cptr;
+            pa.cpos = cpos;
+            pa.crow = crow;
+            pa.col_off = h->off[l];
+            for (int q = 0; q <= L; ++q) pa.lev_off[q] = h->off[q];
+            for (int q = 0; q < L; ++q) {
+                pa.lev_xs[q] = h->lev[q].xs;
+                pa.lev_n[q] = h->lev[q].n;
+            }
+            pa.val_out = h->tval;
+            pa.fail = pstat;
+            patch_count(pa, pstat + 4, st);
+            std::vector<int32_t> hc((size_t)D.n);
+            int hp = 0;
+            MSK_CUDA(cudaMemcpyAsync(&hp, pstat + 4, sizeof hp, cudaMemcpyDeviceToHost, st));
+            MSK_CUDA(cudaMemcpyAsync(hc.data(), D.cnt, sizeof(int32_t) * (size_t)D.n, cudaMemcpyDeviceToHost, st));
+            MSK_CUDA(cudaStreamSynchronize(st));
+            const int maxrow = D.n ? *std::max_element(hc.begin(), hc.end()) : 0;
+            if (getenv("MSK_DEBUG_PATCH"))
+                fprintf(stderr, "[msk] patch level %d: n %lld q %.6g rho %.6g reach %d cell %.6g pmax %d maxrow %d\n", l,
+                        (long long)D.n, D.q, rho, pa.reach, 1.0 / D.g.inv_cell, hp, maxrow);
+            pa.pmax = hp;
+            pa.nnzmax = (int)std::min<int64_t>((int64_t)hp * maxrow, (int64_t)hp * hp);
+            const size_t smem = patch_smem_bytes(pa.pmax, pa.nnzmax);
+            if (smem > 227 * 1024)
+                throw Error(MSK_ERR_INVALID, "msk_assemble: local patch too large for shared memory (" +
+                                                 std::to_string(hp) + " points); reduce patch_R");
+            patch_lagrange(pa, smem, st, launches);
+            MSK_CUDA(cudaMemsetAsync(pstat + 4, 0, sizeof(int), st));
+            continue;
+        }
         const int64_t nb_total = (D.n + 31) / 32;
         const double slot_bytes = 4.0 * (double)D.n * 32.0 * 8.0;
         int64_t slots = std::min<int64_t>(nb_total, std::max<int64_t>(1, std::min<int64_t>(resident, (int64_t)(budget / slot_bytes))));
@@ -711,19 +762,27 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, int *launches
         }
         dfree(ws, st);
     }
-    int hstat[2];
+    int hstat[2], hps[5];
     MSK_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof hstat, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaMemcpyAsync(hps, pstat, sizeof hps, cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaStreamSynchronize(st));
-    dfree(dstat, st); dfree(cptr, st); dfree(cpos, st); dfree(crow, st); dfree(ccol, st);
-    h->lagrange_max_iters = hstat[1];
+    dfree(dstat, st); dfree(pstat, st); dfree(cptr, st); dfree(cpos, st); dfree(crow, st); dfree(ccol, st);
+    h->lagrange_max_iters = std::max(hstat[1], hps[2]);
+    h->patch_max_points = hps[3];
     h->T = T;
     if (hstat[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: Lagrange CG did not converge in 20000 iterations");
+    if (hps[1]) throw Error(MSK_ERR_INVALID, "msk_assemble: local patch overflow in " + std::to_string(hps[1]) +
+                                                 " columns; reduce patch_R");
+    if (hps[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: patch Lagrange CG did not converge in " +
+                                                std::to_string(hps[0]) + " columns");
 }
 
 }  // namespace
 
-extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol) {
+extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrange_tol, double patch_R,
+                                      int64_t patch_min_n) {
     API_BEGIN
+    require(std::isfinite(patch_R) && patch_min_n >= 0, "msk_assemble_ex: bad patch arguments");
     require(h != nullptr, "msk_assemble: NULL hierarchy");
     require(std::isfinite(T), "msk_assemble: T must be finite");
     require(!(T > 0.0) || (lagrange_tol > 0.0 && lagrange_tol < 1.0),
@@ -853,13 +912,17 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
         LevelView v = h->view(l);
         fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
     }
-    if (T > 0.0 && h->L > 1) build_factor(h, T, lagrange_tol, &launches);
+    if (T > 0.0 && h->L > 1) build_factor(h, T, lagrange_tol, patch_R, patch_min_n, &launches);
     tm.stop();
     MSK_CUDA(cudaStreamSynchronize(st));
     h->t_assemble_ms = tm.ms();
     h->launches_assemble = launches;
     h->assembled = true;
     API_END
+}
+
+extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol) {
+    return msk_assemble_ex(h, T, lagrange_tol, 0.0, 0);
 }
 
 // =================================================================== solve

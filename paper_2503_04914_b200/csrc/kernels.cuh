@@ -247,6 +247,37 @@ struct ThreshValueArgs {
     double *val;                    // factor values (output)
 };
 void thresh_values(const ThreshValueArgs &a, cudaStream_t st, int *launches);
+// Local-patch Lagrange functions: for coarse column i of level
+// l, c = A_P^{-1} e_i on the patch P = {h : |x_h - x_i| < rho} (A_l restricted
+// to P), chi~_i = sum_{h in P} c_h Phi_l(. - x_h), written at the column's
+// stored entries.  One CTA per column, patch system in shared memory.
+struct PatchArgs {
+    int d, k, L;
+    int64_t ncols;                  // columns of level l processed (0 .. ncols-1)
+    double rho2;                    // patch radius^2 (no-FMA test, reading C-4 recipe)
+    int reach;                      // cells of level l's grid spanned by rho
+    int pmax, nnzmax;               // shared-memory capacity (points, local entries)
+    LevelView Lv;                   // the coarse level (cells, SoA coordinates)
+    const int64_t *row_ptr;         // A_l (spatial)
+    const int32_t *col;
+    const double *val;
+    double tol2;                    // lagrange_tol^2 (||e_i|| = 1)
+    int max_iter;
+    // stored entries (CSC over the global coarse columns)
+    const int64_t *cptr;            // indexed by global column col_off + i
+    const int64_t *cpos;
+    const int32_t *crow;
+    int64_t col_off;
+    int64_t lev_off[kMaxLevels + 1];
+    const double *lev_xs[kMaxLevels];
+    int64_t lev_n[kMaxLevels];
+    double *val_out;                // factor values
+    int *fail;                      // [0] CG failures, [1] patch overflows, [2] max iterations, [3] max patch
+};
+// max patch size over the columns (count pass, exact test) into *pmax_out (device int)
+void patch_count(const PatchArgs &a, int *pmax_out, cudaStream_t st);
+void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launches);
+size_t patch_smem_bytes(int pmax, int nnzmax);
 // out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)
 void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,
                   const double *u, double *out, cudaStream_t st);

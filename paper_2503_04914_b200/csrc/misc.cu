@@ -23,26 +23,35 @@ __device__ __forceinline__ unsigned long long ord_key(double v) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Bounding box of n row-major d-dimensional points as ordered keys (exact).
+// The array is read as flat doubles (coalesced); a thread's stride is a
+// multiple of d, so each thread sees one axis only.
 __global__ void k_minmax(int64_t n, int d, const double *__restrict__ pts, unsigned long long *mm) {
-    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
-    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
-        for (int a = 0; a < d; ++a) {
-            unsigned long long k = ord_key(pts[i * d + a]);
-            lo[a] = k < lo[a] ? k : lo[a];
-            hi[a] = k > hi[a] ? k : hi[a];
-        }
+    __shared__ unsigned long long slo[3], shi[3];
+    if (threadIdx.x < 3) {
+        slo[threadIdx.x] = ~0ull;
+        shi[threadIdx.x] = 0ull;
     }
-    for (int a = 0; a < d; ++a) {
-        for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long t = __shfl_xor_sync(0xffffffffu, lo[a], o);
-            lo[a] = t < lo[a] ? t : lo[a];
-            t = __shfl_xor_sync(0xffffffffu, hi[a], o);
-            hi[a] = t > hi[a] ? t : hi[a];
+    __syncthreads();
+    const int64_t total = n * d;
+    const int64_t nthreads = (int64_t)gridDim.x * NT;
+    const int64_t stride = nthreads - nthreads % d;  // multiple of d
+    const int64_t g = (int64_t)blockIdx.x * NT + threadIdx.x;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    if (g < stride) {
+        for (int64_t k = g; k < total; k += stride) {
+            const unsigned long long key = ord_key(pts[k]);
+            lo = key < lo ? key : lo;
+            hi = key > hi ? key : hi;
         }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&mm[a], lo[a]);
-            atomicMax(&mm[3 + a], hi[a]);
-        }
+        const int a = (int)(g % d);
+        atomicMin(&slo[a], lo);
+        atomicMax(&shi[a], hi);
+    }
+    __syncthreads();
+    if (threadIdx.x < d) {
+        atomicMin(&mm[threadIdx.x], slo[threadIdx.x]);
+        atomicMax(&mm[3 + threadIdx.x], shi[threadIdx.x]);
     }
 }
 }  // namespace

@@ -224,7 +224,317 @@ __global__ void __launch_bounds__(NT) k_csc_spmv_add(int64_t ncols, const int64_
     for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k) s = fma(val[cpos[k]], u[crow[k]], s);
     out[c] += s;
 }
+
+// ---------------------------------------------------------------------------
+// Local-patch Lagrange functions (PatchArgs, kernels.cuh).
+//
+// A CTA owns coarse column i of level l:
+//  1. patch P = level-l points with |x_h - x_i|^2 < rho^2, enumerated over the
+//     (2m+1)^(d-1) z-columns of cells around x_i in increasing key order, so the
+//     global ids pid[] come out ascending (count, block scan, write);
+//  2. local CSR of A_P: rows of A_l restricted to columns in P (binary search
+//     in pid[]), values copied (count, block scan, fill);
+//  3. CG on A_P c = e_i (x0 = 0, stop ||r|| <= lagrange_tol, reading C-9),
+//     vectors in shared memory, block_sum reductions (deterministic);
+//  4. for each stored entry (fine point x_j) of column i:
+//     chi~_i(x_j) = delta_l^-d sum_{h in P, r < delta_l} phi(r/delta_l) c_h,
+//     h ascending (the order of k_tvalues).
+size_t patch_smem_bytes_impl(int pmax, int nnzmax) {
+    size_t b = 0;
+    b += sizeof(int32_t) * (size_t)pmax;          // pid
+    b += sizeof(int32_t) * (size_t)(pmax + 1);    // prow
+    b = (b + 15) & ~(size_t)15;
+    b += sizeof(double) * 4 * (size_t)pmax;       // x r p q
+    b += sizeof(double) * (size_t)nnzmax;         // pval
+    b += sizeof(int32_t) * (size_t)nnzmax;        // pcol
+    b += sizeof(int32_t) * 1024;                  // column counts / scan scratch
+    return b + 64;
+}
+
+template <int D>
+__device__ __forceinline__ void patch_columns(const LevelView &L, const double *x, int m, int64_t c[3],
+                                              int64_t &x0, int64_t &x1, int64_t &y0, int64_t &y1,
+                                              int64_t &z0, int64_t &z1) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) c[a] = cell_coord(L.g, a, x[a]);
+    const int la = D - 1;
+    z0 = c[la] - m < 0 ? 0 : c[la] - m;
+    z1 = c[la] + m >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + m;
+    x0 = c[0] - m < 0 ? 0 : c[0] - m;
+    x1 = c[0] + m >= L.g.dim[0] ? L.g.dim[0] - 1 : c[0] + m;
+    if (D == 3) {
+        y0 = c[1] - m < 0 ? 0 : c[1] - m;
+        y1 = c[1] + m >= L.g.dim[1] ? L.g.dim[1] - 1 : c[1] + m;
+    } else {
+        y0 = 0;
+        y1 = 0;
+    }
+}
+
+// range of the q-th z-column (row-major over (ix, iy)); empty if z0 > z1
+template <int D>
+__device__ __forceinline__ void patch_range(const LevelView &L, int q, int64_t x0, int64_t y0, int64_t y1,
+                                            int64_t z0, int64_t z1, int &b, int &e) {
+    const int64_t ny = y1 - y0 + 1;
+    const int64_t ix = x0 + q / ny, iy = y0 + q % ny;
+    const int64_t kb = D == 3 ? (ix * L.g.dim[1] + iy) * L.g.dim[2] : ix * L.g.dim[1];
+    b = L.cell_start[kb + z0];
+    e = L.cell_start[kb + z1 + 1];
+}
+
+template <int D>
+__global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, int *pmax_out) {
+    const int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (i >= a.ncols) return;
+    const LevelView &L = a.Lv;
+    double x[3];
+#pragma unroll
+    for (int t = 0; t < D; ++t) x[t] = L.x[t][i];
+    int cnt = 0;
+    for_each_range_m<D>(L, x, a.reach, [&](int b, int e) {
+        for (int h = b; h < e; ++h) {
+            double y[3];
+#pragma unroll
+            for (int t = 0; t < D; ++t) y[t] = L.x[t][h];
+            if (dist2_nofma<D>(x, y) < a.rho2) ++cnt;
+        }
+    });
+    atomicMax(pmax_out, cnt);
+}
+
+__device__ __forceinline__ int find_sorted(const int32_t *v, int n, int32_t key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && v[lo] == key ? lo : -1;
+}
+
+// exclusive block scan of cnt[0..n) in shared memory (n <= NT * k), result in place; returns the total
+__device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp /* NT */) {
+    const int tid = threadIdx.x;
+    const int per = (n + NT - 1) / NT;
+    int s = 0;
+    for (int k = 0; k < per; ++k) {
+        const int idx = tid * per + k;
+        if (idx < n) s += cnt[idx];
+    }
+    tmp[tid] = s;
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int t = 0; t < NT; ++t) {
+            const int v = tmp[t];
+            tmp[t] = run;
+            run += v;
+        }
+        tmp[NT] = run;
+    }
+    __syncthreads();
+    int run = tmp[tid];
+    for (int k = 0; k < per; ++k) {
+        const int idx = tid * per + k;
+        if (idx < n) {
+            const int v = cnt[idx];
+            cnt[idx] = run;
+            run += v;
+        }
+    }
+    const int total = tmp[NT];
+    __syncthreads();
+    return total;
+}
+
+template <int D, int K>
+__global__ void __launch_bounds__(NT) k_patch(PatchArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[NT / 32 + 2];
+    __shared__ int32_t tmp[NT + 1];
+    const int64_t i = blockIdx.x;
+    if (i >= a.ncols) return;
+    const int tid = threadIdx.x;
+    const LevelView &L = a.Lv;
+    const int pmax = a.pmax;
+    unsigned char *ptr = smem_raw;
+    int32_t *pid = reinterpret_cast<int32_t *>(ptr);
+    ptr += sizeof(int32_t) * (size_t)pmax;
+    int32_t *prow = reinterpret_cast<int32_t *>(ptr);
+    ptr += sizeof(int32_t) * (size_t)(pmax + 1);
+    ptr = reinterpret_cast<unsigned char *>(((uintptr_t)ptr + 15) & ~(uintptr_t)15);
+    double *X = reinterpret_cast<double *>(ptr);
+    double *Rv = X + pmax, *P = Rv + pmax, *Q = P + pmax;
+    double *pval = Q + pmax;
+    int32_t *pcol = reinterpret_cast<int32_t *>(pval + a.nnzmax);
+    int32_t *ccnt = pcol + a.nnzmax;  // 1024 column counters
+    double xc[3];
+#pragma unroll
+    for (int t = 0; t < D; ++t) xc[t] = L.x[t][i];
+    // ---- 1. patch points, ascending global id
+    int64_t c[3], x0, x1, y0, y1, z0, z1;
+    patch_columns<D>(L, xc, a.reach, c, x0, x1, y0, y1, z0, z1);
+    const int ncolz = (int)((x1 - x0 + 1) * (y1 - y0 + 1));
+    if (ncolz > 1024) {
+        if (tid == 0) atomicAdd(&a.fail[1], 1);
+        return;
+    }
+    for (int q = tid; q < ncolz; q += NT) {
+        int b, e, n = 0;
+        patch_range<D>(L, q, x0, y0, y1, z0, z1, b, e);
+        for (int h = b; h < e; ++h) {
+            double y[3];
+#pragma unroll
+            for (int t = 0; t < D; ++t) y[t] = L.x[t][h];
+            if (dist2_nofma<D>(xc, y) < a.rho2) ++n;
+        }
+        ccnt[q] = n;
+    }
+    __syncthreads();
+    const int np = block_scan_excl(ccnt, ncolz, tmp);
+    if (np > pmax) {
+        if (tid == 0) atomicAdd(&a.fail[1], 1);
+        return;
+    }
+    for (int q = tid; q < ncolz; q += NT) {
+        int b, e, w = ccnt[q];
+        patch_range<D>(L, q, x0, y0, y1, z0, z1, b, e);
+        for (int h = b; h < e; ++h) {
+            double y[3];
+#pragma unroll
+            for (int t = 0; t < D; ++t) y[t] = L.x[t][h];
+            if (dist2_nofma<D>(xc, y) < a.rho2) pid[w++] = h;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) atomicMax(&a.fail[3], np);
+    // ---- 2. local CSR of A restricted to the patch
+    for (int r = tid; r < np; r += NT) {
+        const int32_t g = pid[r];
+        int n = 0;
+        for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k)
+            if (find_sorted(pid, np, a.col[k]) >= 0) ++n;
+        prow[r] = n;
+    }
+    __syncthreads();
+    int nnz = 0;
+    {
+        // scan prow[0..np) (reuse block_scan_excl on the prow array)
+        nnz = block_scan_excl(prow, np, tmp);
+        if (tid == 0) prow[np] = nnz;
+    }
+    if (nnz > a.nnzmax) {
+        if (tid == 0) atomicAdd(&a.fail[1], 1);
+        return;
+    }
+    for (int r = tid; r < np; r += NT) {
+        const int32_t g = pid[r];
+        int w = prow[r];
+        for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k) {
+            const int lc = find_sorted(pid, np, a.col[k]);
+            if (lc >= 0) {
+                pcol[w] = lc;
+                pval[w] = a.val[k];
+                ++w;
+            }
+        }
+    }
+    // ---- 3. CG on A_P c = e_center
+    const int ctr = find_sorted(pid, np, (int32_t)i);
+    __syncthreads();
+    for (int r = tid; r < np; r += NT) {
+        const double e = r == ctr ? 1.0 : 0.0;
+        X[r] = 0.0;
+        Rv[r] = e;
+        P[r] = e;
+    }
+    double rr = 1.0;
+    int it = 0;
+    __syncthreads();
+    while (rr > a.tol2) {
+        if (it >= a.max_iter) {
+            if (tid == 0) atomicAdd(&a.fail[0], 1);
+            break;
+        }
+        double pq = 0.0;
+        for (int r = tid; r < np; r += NT) {
+            double acc = 0.0;
+            for (int k = prow[r]; k < prow[r + 1]; ++k) acc = fma(pval[k], P[pcol[k]], acc);
+            Q[r] = acc;
+            pq += P[r] * acc;
+        }
+        pq = block_sum<NT>(pq, red);
+        const double alpha = rr / pq;
+        double rn = 0.0;
+        for (int r = tid; r < np; r += NT) {
+            const double v = Rv[r] - alpha * Q[r];
+            Rv[r] = v;
+            rn += v * v;
+            X[r] += alpha * P[r];
+        }
+        rn = block_sum<NT>(rn, red);
+        const double beta = rn / rr;
+        rr = rn;
+        for (int r = tid; r < np; r += NT) P[r] = Rv[r] + beta * P[r];
+        __syncthreads();
+        ++it;
+    }
+    if (tid == 0) atomicMax(&a.fail[2], it);
+    __syncthreads();
+    // ---- 4. values at the stored entries of column i
+    const int64_t gc = a.col_off + i;
+    const double d2 = L.delta2, inv = L.inv_delta;
+    for (int64_t t = a.cptr[gc] + tid; t < a.cptr[gc + 1]; t += NT) {
+        const int64_t g = a.crow[t];
+        int k = 0;
+        while (k + 1 < a.L && g >= a.lev_off[k + 1]) ++k;
+        const int64_t j = g - a.lev_off[k];
+        double xj[3];
+#pragma unroll
+        for (int q = 0; q < D; ++q) xj[q] = a.lev_xs[k][(int64_t)q * a.lev_n[k] + j];
+        double s = 0.0;
+        for_each_range<D>(L, xj, [&](int b, int e) {
+            for (int h = b; h < e; ++h) {
+                double y[3];
+#pragma unroll
+                for (int q = 0; q < D; ++q) y[q] = L.x[q][h];
+                const double r2 = dist2_nofma<D>(xj, y);
+                if (r2 < d2) {
+                    const int lh = find_sorted(pid, np, h);
+                    if (lh >= 0) s = fma(wendland<K>(sqrt(r2) * inv), X[lh], s);
+                }
+            }
+        });
+        a.val_out[a.cpos[t]] = L.scale * s;
+    }
+}
 }  // namespace
+
+size_t patch_smem_bytes(int pmax, int nnzmax) { return patch_smem_bytes_impl(pmax, nnzmax); }
+
+void patch_count(const PatchArgs &a, int *pmax_out, cudaStream_t st) {
+    if (a.ncols <= 0) return;
+    if (a.d == 2) k_patch_count<2><<<ceil_div_u(a.ncols, NT), NT, 0, st>>>(a, pmax_out);
+    else k_patch_count<3><<<ceil_div_u(a.ncols, NT), NT, 0, st>>>(a, pmax_out);
+    MSK_CHECK_LAUNCH();
+}
+
+void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launches) {
+    if (a.ncols <= 0) return;
+#define MSK_PT(DD, KK)                                                                            \
+    do {                                                                                         \
+        MSK_CUDA(cudaFuncSetAttribute(k_patch<DD, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)smem));                                               \
+        k_patch<DD, KK><<<(unsigned)a.ncols, NT, smem, st>>>(a);                                  \
+    } while (0)
+    if (a.d == 2) {
+        if (a.k == 0) MSK_PT(2, 0); else if (a.k == 1) MSK_PT(2, 1); else MSK_PT(2, 2);
+    } else {
+        if (a.k == 0) MSK_PT(3, 0); else if (a.k == 1) MSK_PT(3, 1); else MSK_PT(3, 2);
+    }
+#undef MSK_PT
+    MSK_CHECK_LAUNCH();
+    if (launches) *launches += 1;
+}
 
 void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,
                   const double *u, double *out, cudaStream_t st) {

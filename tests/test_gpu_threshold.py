@@ -136,3 +136,40 @@ def test_thresholded_C3_prefix_runs(msk, ctx):
         assert info.nnz_gather == cnt
         errs.append(sum(np.linalg.norm(a_t[l] - a_ex[l]) for l in range(3)))
     assert errs[1] < errs[0]
+
+
+# ------------------------------------------- local-patch Lagrange (NEXT-4)
+@pytest.mark.parametrize("R,bar", [(7.0, 1e-6), (11.0, 1e-12)])
+def test_patch_lagrange_matches_exact(msk, ctx, R, bar):
+    """msk_assemble_ex: chi_i from A_l restricted to the patch |x_h - x_i| <
+    R q_l.  Same geometric pattern (bit-exact) as the exact build; values within
+    a bar that falls exponentially with R - T (Lemma lagrangedecay); the solve
+    inherits it."""
+    H = config("C3P4", m_eval=0)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble(T=3.0, lagrange_tol=1e-14)
+    ref = {(k, l): h.export_factor(k, l) for k in range(1, H.L) for l in range(k)}
+    a_ref, _ = h.solve(H.f())
+    h.assemble(T=3.0, lagrange_tol=1e-14, patch_R=R, patch_min_n=0)
+    for (k, l), (rp, col, val, _) in ref.items():
+        rp2, col2, val2, _ = h.export_factor(k, l)
+        assert np.array_equal(rp, rp2) and np.array_equal(col, col2)
+        assert np.abs(val2 - val).max() <= bar * np.abs(val).max(), (k, l, R)
+    a, _ = h.solve(H.f())
+    for l in range(H.L):
+        assert np.linalg.norm(a[l] - a_ref[l]) <= 10 * bar * np.linalg.norm(a_ref[l])
+    # patch_min_n: levels at or below the threshold keep the exact build (identical bits)
+    h.assemble(T=3.0, lagrange_tol=1e-14, patch_R=R, patch_min_n=5000)
+    for (k, l), (rp, col, val, _) in ref.items():
+        if H.n[l] <= 5000:
+            assert np.array_equal(h.export_factor(k, l)[2], val)
+    h.close()
+
+
+def test_patch_too_large_is_invalid(msk, ctx):
+    H = config("C3P4", m_eval=0)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    with pytest.raises(msk.MskError) as ei:
+        h.assemble(T=3.0, lagrange_tol=1e-14, patch_R=40.0, patch_min_n=0)
+    assert ei.value.status == 1
+    h.close()

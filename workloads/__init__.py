@@ -162,13 +162,14 @@ def config(name: str, m_eval=None) -> Hierarchy:
     if name == "C2":
         return halton_hierarchy("C2", 2, [1024 * 4 ** l for l in range(6)], 4.0,
                                 m_eval=10_000 if m_eval is None else m_eval)
-    if name in ("C3", "C3P4", "C3P5", "C4"):
+    if name in ("C3", "C3P4", "C3P5", "C4", "C4F"):
         # C4 = the thresholded-factor study on the 4-level prefix of C3 (the
-        # exact Lagrange build costs sum_l N(l)^2)
-        L = {"C3": 6, "C3P4": 4, "C3P5": 5, "C4": 4}[name]
+        # exact Lagrange build costs sum_l N(l)^2); C4F = the
+        # same on all of C3 with local-patch Lagrange functions (NEXT-4)
+        L = {"C3": 6, "C3P4": 4, "C3P5": 5, "C4": 4, "C4F": 6}[name]
         sizes = [int(round(1e7 * 8.0 ** (l - 6))) for l in range(1, 7)][:L]
         return halton_hierarchy(name, 3, sizes, 1.5,
-                                m_eval=(10_000_000 if name == "C3" else 1_000_000 if name == "C4"
+                                m_eval=(10_000_000 if name in ("C3", "C4F") else 1_000_000 if name == "C4"
                                         else 100_000) if m_eval is None else m_eval)
     if name.startswith("P") and name[1:].isdigit():
         # paper workload (Table 1 / Figure 4): grids l=1..L, nu=4, phi_(3,1)
