@@ -85,8 +85,25 @@ __global__ void __launch_bounds__(NT, MSK_GMINB) k_gather(GatherArgs a) {
                 nh = 0;
             };
             for_each_range<D>(L, x, [&](int b, int e) {
-                // conservative FP32 prefilter on 16-byte records; 2 candidates per trip
+                // conservative FP32 prefilter on 16-byte records; 4 candidates per
+                // trip (independent loads in flight: eval 6.21 -> 5.94 ms), then 2, then 1
                 int j = b;
+                for (; j + 3 < e; j += 4) {
+                    const float4 F0 = frec[j], F1 = frec[j + 1], F2 = frec[j + 2], F3 = frec[j + 3];
+                    float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    float a1 = xf[0] - F1.x, b1 = xf[1] - F1.y, c1 = xf[2] - F1.z;
+                    float a2 = xf[0] - F2.x, b2 = xf[1] - F2.y, c2 = xf[2] - F2.z;
+                    float a3 = xf[0] - F3.x, b3 = xf[1] - F3.y, c3 = xf[2] - F3.z;
+                    const bool h0 = fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr;
+                    const bool h1 = fmaf(c1, c1, fmaf(b1, b1, a1 * a1)) < fthr;
+                    const bool h2 = fmaf(c2, c2, fmaf(b2, b2, a2 * a2)) < fthr;
+                    const bool h3 = fmaf(c3, c3, fmaf(b3, b3, a3 * a3)) < fthr;
+                    if (nh + 4 > HMAX) flush();
+                    if (h0) hl[nh++] = j;
+                    if (h1) hl[nh++] = j + 1;
+                    if (h2) hl[nh++] = j + 2;
+                    if (h3) hl[nh++] = j + 3;
+                }
                 for (; j + 1 < e; j += 2) {
                     const float4 F0 = frec[j], F1 = frec[j + 1];
                     float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
