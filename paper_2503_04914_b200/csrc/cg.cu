@@ -52,8 +52,6 @@ namespace msk {
 namespace {
 constexpr int NT = 256;       // threads per CTA == rows per tile
 constexpr int NW = NT / 32;   // warps per CTA
-constexpr int CAPW = 224;     // CSR entries per warp pipeline stage (values 1.75 KB + columns 0.9 KB)
-constexpr int CAPWE = CAPW - 2;  // usable entries per stage (16-byte alignment slack)
 #ifndef MSK_U
 #define MSK_U 4
 #endif
@@ -70,19 +68,6 @@ constexpr int RPCAP = MAXCH * NT + 4;  // staged row pointers per chunk
 struct CGBatch {
     int nlev;
     CGLevelArgs lev[kMaxLevels];
-};
-
-struct __align__(16) WarpStage {
-    double val[CAPW];         // values, overwritten in place by the products
-    int32_t col[CAPW + 8];
-};
-
-struct __align__(16) CGShared {
-    WarpStage st[NW][2];      // per-warp double-buffered CSR slices
-    int64_t rp[RPCAP];        // row pointers of the current chunk
-    double red[NT / 32 + 2];
-    uint64_t bar;             // CTA barrier for the row-pointer copy
-    uint64_t wbar[NW][2];     // per-warp, per-stage barriers
 };
 
 // ---- CTA-level pipeline (used by k_cg): large bulk copies, double-buffered.
@@ -142,154 +127,6 @@ __device__ __forceinline__ double chunk_allreduce(const double *partials, int64_
     double t = 0.0;
     for (int64_t j = threadIdx.x; j < nchunks; j += NT) t += __ldcg(&partials[j]);
     return block_sum<NT>(t, s_red);
-}
-
-// Stage row pointers of rows [r0, r0 + nrows] (nrows + 1 entries) into
-// S.rp; returns the offset of row r0 inside S.rp.  Whole CTA calls.
-__device__ __forceinline__ int stage_row_ptr(CGShared &S, const int64_t *row_ptr, int64_t r0,
-                                             int nrows, uint32_t &phase, uint64_t pol) {
-    const int64_t lo = r0 & ~(int64_t)1;
-    const int64_t hi = (r0 + nrows + 2) & ~(int64_t)1;  // exclusive, even
-    if (threadIdx.x == 0) {
-        uint32_t bytes = (uint32_t)((hi - lo) * 8);
-        mbar_arrive_expect_tx(&S.bar, bytes);
-        tma_load_1d(S.rp, row_ptr + lo, bytes, &S.bar, pol);
-    }
-    mbar_wait(&S.bar, phase);
-    phase ^= 1u;
-    return (int)(r0 - lo);
-}
-
-// Issue the bulk copies of CSR entries [kb, ke) into a warp stage (lane 0).
-__device__ __forceinline__ void issue_piece(WarpStage &stg, uint64_t *bar, const int32_t *col,
-                                            const double *val, int64_t kb, int64_t ke,
-                                            uint64_t pol) {
-    const int64_t vlo = kb & ~(int64_t)1, vhi = (ke + 1) & ~(int64_t)1;
-    const int64_t clo = kb & ~(int64_t)3, chi = (ke + 3) & ~(int64_t)3;
-    const uint32_t vb = (uint32_t)((vhi - vlo) * 8), cb = (uint32_t)((chi - clo) * 4);
-    mbar_arrive_expect_tx(bar, vb + cb);
-    tma_load_1d(stg.val, val + vlo, vb, bar, pol);
-    tma_load_1d(stg.col, col + clo, cb, bar, pol);
-}
-
-// Warp-level pipelined SpMV: q_i = (A p)_i for the warp's rows
-// [wr0, wr0 + nrows) whose row pointers sit at S.rp[ro ...].  The rows are
-// cut into subtiles of 32 (lane == row) and the subtiles' CSR slices into
-// pieces of <= CAPWE entries; piece j+1 is copied (TMA) into the other
-// stage while piece j is processed.  Lanes gather p[col] for the piece's
-// entries (strided, U loads in flight), multiply in place, then each lane
-// sums its own row in ascending column order.  Returns the lane's share
-// of p.q over its rows.  J counts the warp's pieces over the whole launch:
-// piece J uses stage J&1 and completes its barrier phase with parity
-// (J>>1)&1.
-__device__ __forceinline__ double spmv_warp(CGShared &S, int ro, int nrows, int64_t wr0,
-                                            const int32_t *col, const double *val, const double *p,
-                                            double *q, uint32_t &J, uint64_t pol) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    WarpStage *stg = S.st[w];
-    uint64_t *bars = S.wbar[w];
-    double dot = 0.0;
-    if (nrows <= 0) return 0.0;
-    const int nsub = (nrows + 31) >> 5;
-    // piece cursor: subtile s, entries [kb, ke)
-    int s = 0;
-    int64_t sub_end = S.rp[ro + (nrows < 32 ? nrows : 32)];
-    int64_t kb = S.rp[ro];
-    int64_t ke = kb + CAPWE < sub_end ? kb + CAPWE : sub_end;
-    if (lane == 0) issue_piece(stg[J & 1], &bars[J & 1], col, val, kb, ke, pol);
-    int64_t myb = lane < nrows ? S.rp[ro + lane] : 0, mye = lane < nrows ? S.rp[ro + lane + 1] : 0;
-    double acc = 0.0;
-    for (uint32_t j = J;; ++j) {
-        // next piece
-        int s2 = s;
-        int64_t kb2 = ke, ke2 = 0, sub_end2 = sub_end;
-        if (ke == sub_end) {
-            s2 = s + 1;
-            if (s2 < nsub) {
-                int re = (s2 + 1) * 32 < nrows ? (s2 + 1) * 32 : nrows;
-                sub_end2 = S.rp[ro + re];
-            }
-        }
-        const bool has_next = s2 < nsub;
-        if (has_next) ke2 = kb2 + CAPWE < sub_end2 ? kb2 + CAPWE : sub_end2;
-        // stage (j+1)&1 held piece j-1, fully consumed (fence + syncwarp at its end)
-        if (has_next && lane == 0) issue_piece(stg[(j + 1) & 1], &bars[(j + 1) & 1], col, val, kb2, ke2, pol);
-        const int sj = (int)(j & 1u);
-        mbar_wait(&bars[sj], (j >> 1) & 1u);
-        WarpStage &cur = stg[sj];
-        const int voff = (int)(kb & 1), coff = (int)(kb & 3);
-        {
-            // row-parallel: each lane gathers its own row's columns of this
-            // piece (U independent loads in flight), ascending column order
-            const int64_t lo64 = myb > kb ? myb : kb, hi64 = mye < ke ? mye : ke;  // 64-bit clamp
-            const int lo = (int)(lo64 - kb), hi = hi64 > lo64 ? (int)(hi64 - kb) : lo;
-            for (int e = lo; e < hi; e += U) {
-                double pv[U], vv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int ee = e + u;
-                    pv[u] = ee < hi ? p[cur.col[coff + ee]] : 0.0;
-                    vv[u] = ee < hi ? cur.val[voff + ee] : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (e + u < hi) acc = fma(vv[u], pv[u], acc);
-            }
-        }
-        if (ke == sub_end) {  // subtile s complete
-            const int lr = s * 32 + lane;
-            if (lr < nrows) {
-                const int64_t i = wr0 + lr;
-                q[i] = acc;
-                dot += p[i] * acc;
-            }
-            acc = 0.0;
-            if (has_next) {
-                const int lr2 = s2 * 32 + lane;
-                myb = lr2 < nrows ? S.rp[ro + lr2] : 0;
-                mye = lr2 < nrows ? S.rp[ro + lr2 + 1] : 0;
-            }
-        }
-        fence_proxy_async_smem();  // generic writes to this stage before its next TMA refill
-        __syncwarp();
-        if (!has_next) {
-            J = j + 1;
-            break;
-        }
-        s = s2;
-        kb = kb2;
-        ke = ke2;
-        sub_end = sub_end2;
-    }
-    return dot;
-}
-
-__device__ __forceinline__ void init_barriers(CGShared &S) {
-    if ((threadIdx.x & 31) == 0) {
-        const int w = threadIdx.x >> 5;
-        mbar_init(&S.wbar[w][0], 1);
-        mbar_init(&S.wbar[w][1], 1);
-        if (w == 0) mbar_init(&S.bar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-}
-
-// q = A p over one chunk of rows [cr0, cr0 + crows): row pointers staged by
-// the CTA, then each warp runs its pipelined SpMV over its contiguous rows.
-// Returns the thread's share of p.q.
-__device__ __forceinline__ double spmv_chunk(CGShared &S, const int64_t *row_ptr, const int32_t *col,
-                                             const double *val, const double *p, double *q,
-                                             int64_t cr0, int crows, int CH, uint32_t &phase,
-                                             uint32_t &J, uint64_t pol) {
-    const int ro = stage_row_ptr(S, row_ptr, cr0, crows, phase, pol);
-    const int w = threadIdx.x >> 5;
-    const int per = 32 * CH;
-    const int w0 = w * per;
-    const int wn = crows - w0 < per ? crows - w0 : per;
-    double dot = spmv_warp(S, ro + w0, wn, cr0 + w0, col, val, p, q, J, pol);
-    __syncthreads();  // S.rp is reused by the next chunk's copy
-    return dot;
 }
 
 // ---------------------------------------------------------------------------
@@ -968,22 +805,6 @@ __global__ void __launch_bounds__(NT, MB) k_spmv_t(CGLevelArgs L, int CH) {
                         0.0);
 }
 
-// (superseded warp-pipelined standalone SpMV, kept for reference timings)
-__global__ void __launch_bounds__(NT) k_spmv(int64_t n, const int64_t *__restrict__ row_ptr,
-                                             const int32_t *__restrict__ col,
-                                             const double *__restrict__ val,
-                                             const double *__restrict__ v, double *__restrict__ y) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    CGShared &S = *reinterpret_cast<CGShared *>(smem_raw);
-    uint32_t phase = 0;
-    uint32_t J = 0;  // pieces consumed by this warp
-    init_barriers(S);
-    const uint64_t pol = policy_evict_first();
-    int64_t r0 = (int64_t)blockIdx.x * NT;
-    int nr = (int)(n - r0 < NT ? n - r0 : NT);
-    spmv_chunk(S, row_ptr, col, val, v, y, r0, nr, 1, phase, J, pol);
-}
-
 // ---------------------------------------------------------------------------
 // Distributed CG (one partition = a contiguous range of whole chunks of one
 // level).  The same arithmetic as k_cg, split into phase kernels so that the
@@ -1250,7 +1071,6 @@ void set_smem_attrs() {
         MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, v.cg, NT, v.smem));
         v.resident = sms * (per > 0 ? per : 1);
     }
-    MSK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CGShared)));
     done = true;
 }
 
