@@ -656,7 +656,7 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     int64_t *cptr = dalloc<int64_t>((size_t)(ncols + 1), st);
     int64_t *cpos = dalloc<int64_t>((size_t)nnz, st);
     int32_t *crow = dalloc<int32_t>((size_t)nnz, st);
-    int32_t *ccol = dalloc<int32_t>((size_t)nnz, st);
+    int32_t *ccol = nullptr;  // columns are found by binary search in cptr (saves 4 B per entry)
     thresh_csc(ntot - h->off[1], h->off[1], nnz, ncols, h->trow_ptr, h->tcol, cptr, cpos, crow, ccol, st,
                launches);
     std::vector<int64_t> hcptr((size_t)(ncols + 1));
@@ -711,9 +711,10 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             pa.pmax = hp;
             pa.nnzmax = (int)std::min<int64_t>((int64_t)hp * maxrow, (int64_t)hp * hp);
             const size_t smem = patch_smem_bytes(pa.pmax, pa.nnzmax);
-            if (smem > 227 * 1024)
-                throw Error(MSK_ERR_INVALID, "msk_assemble: local patch too large for shared memory (" +
-                                                 std::to_string(hp) + " points); reduce patch_R");
+            // larger patches run from a global workspace (patch_lagrange); bound it
+            if (smem > (size_t)1 << 30)
+                throw Error(MSK_ERR_INVALID, "msk_assemble: local patch too large (" + std::to_string(hp) +
+                                                 " points); reduce patch_R");
             patch_lagrange(pa, smem, st, launches);
             MSK_CUDA(cudaMemsetAsync(pstat + 4, 0, sizeof(int), st));
             continue;
@@ -747,7 +748,9 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             v.pos1 = hcptr[h->off[l] + c1];
             v.cpos = cpos;
             v.crow = crow;
-            v.ccol = ccol;
+            v.cptr = cptr;
+            v.c_lo = h->off[l] + c0;
+            v.c_hi = h->off[l] + c1;
             v.col_off = (int32_t)h->off[l];
             v.first_col = c0;
             for (int q = 0; q <= L; ++q) v.lev_off[q] = h->off[q];
@@ -1888,7 +1891,6 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
         cptr = dalloc<int64_t>((size_t)(ncols + 1), st);
         cpos = dalloc<int64_t>((size_t)h->tnnz + 1, st);
         crow = dalloc<int32_t>((size_t)h->tnnz + 1, st);
-        ccol = dalloc<int32_t>((size_t)h->tnnz + 1, st);
         thresh_csc(N - h->off[1], h->off[1], h->tnnz, ncols, h->trow_ptr, h->tcol, cptr, cpos, crow, ccol, st,
                    nullptr);
         nv = dalloc<double>((size_t)N, st);

@@ -236,7 +236,8 @@ struct ThreshValueArgs {
     int64_t pos0, pos1;             // CSC positions of this round's columns
     const int64_t *cpos;
     const int32_t *crow;
-    const int32_t *ccol;
+    const int64_t *cptr;            // CSC column starts (global coarse columns)
+    int64_t c_lo, c_hi;             // global columns of this round: positions [cptr[c_lo], cptr[c_hi])
     int32_t col_off;                // global column offset of the coarse level
     int64_t first_col;              // first (level-local) column of this round
     int64_t lev_off[kMaxLevels + 1];

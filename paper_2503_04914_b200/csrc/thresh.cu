@@ -171,7 +171,14 @@ __global__ void __launch_bounds__(NT) k_tvalues(ThreshValueArgs a) {
     const int64_t t = a.pos0 + (int64_t)blockIdx.x * NT + threadIdx.x;
     if (t >= a.pos1) return;
     const int64_t g = a.crow[t];                 // global row (point of a finer level)
-    const int32_t c = a.ccol[t] - a.col_off;     // column inside level l
+    // column of CSC position t: the largest global column c in [c_lo, c_hi) with
+    // cptr[c] <= t (empty columns share their start with the next one)
+    int64_t lo = a.c_lo, hi = a.c_hi;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a.cptr[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int32_t c = (int32_t)(lo - a.col_off);  // column inside level l
     int k = 0;
     while (k + 1 < a.L && g >= a.lev_off[k + 1]) ++k;
     const int64_t j = g - a.lev_off[k];
@@ -346,17 +353,16 @@ __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp
     return total;
 }
 
+// one column; `base` = the CTA's workspace (shared memory, or a global slice
+// for patches that do not fit); every early return is CTA-uniform
 template <int D, int K>
-__global__ void __launch_bounds__(NT) k_patch(PatchArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsigned char *base) {
     __shared__ double red[NT / 32 + 2];
     __shared__ int32_t tmp[NT + 1];
-    const int64_t i = blockIdx.x;
-    if (i >= a.ncols) return;
     const int tid = threadIdx.x;
     const LevelView &L = a.Lv;
     const int pmax = a.pmax;
-    unsigned char *ptr = smem_raw;
+    unsigned char *ptr = base;
     int32_t *pid = reinterpret_cast<int32_t *>(ptr);
     ptr += sizeof(int32_t) * (size_t)pmax;
     int32_t *prow = reinterpret_cast<int32_t *>(ptr);
@@ -507,6 +513,16 @@ __global__ void __launch_bounds__(NT) k_patch(PatchArgs a) {
         a.val_out[a.cpos[t]] = L.scale * s;
     }
 }
+
+template <int D, int K>
+__global__ void __launch_bounds__(NT) k_patch(PatchArgs a, unsigned char *gws, size_t gstride) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char *base = gws ? gws + (size_t)blockIdx.x * gstride : smem_raw;
+    for (int64_t i = blockIdx.x; i < a.ncols; i += gridDim.x) {
+        patch_column<D, K>(a, i, base);
+        __syncthreads();  // the workspace is reused by the next column
+    }
+}
 }  // namespace
 
 size_t patch_smem_bytes(int pmax, int nnzmax) { return patch_smem_bytes_impl(pmax, nnzmax); }
@@ -520,11 +536,23 @@ void patch_count(const PatchArgs &a, int *pmax_out, cudaStream_t st) {
 
 void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launches) {
     if (a.ncols <= 0) return;
+    // a patch that does not fit in shared memory: a global workspace slice per
+    // CTA of a persistent grid (slower, L2-resident vectors)
+    const bool global = smem > 227 * 1024;
+    unsigned grid = (unsigned)a.ncols;
+    unsigned char *gws = nullptr;
+    const size_t stride = (smem + 255) & ~(size_t)255;
+    if (global) {
+        grid = (unsigned)(a.ncols < 148 * 4 ? a.ncols : 148 * 4);
+        MSK_CUDA(cudaMallocAsync((void **)&gws, stride * grid, st));
+    }
+    const size_t dyn = global ? 0 : smem;
 #define MSK_PT(DD, KK)                                                                            \
     do {                                                                                         \
-        MSK_CUDA(cudaFuncSetAttribute(k_patch<DD, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                      (int)smem));                                               \
-        k_patch<DD, KK><<<(unsigned)a.ncols, NT, smem, st>>>(a);                                  \
+        if (!global)                                                                             \
+            MSK_CUDA(cudaFuncSetAttribute(k_patch<DD, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                          (int)smem));                                           \
+        k_patch<DD, KK><<<grid, NT, dyn, st>>>(a, gws, stride);                                  \
     } while (0)
     if (a.d == 2) {
         if (a.k == 0) MSK_PT(2, 0); else if (a.k == 1) MSK_PT(2, 1); else MSK_PT(2, 2);
@@ -533,6 +561,7 @@ void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launc
     }
 #undef MSK_PT
     MSK_CHECK_LAUNCH();
+    if (gws) MSK_CUDA(cudaFreeAsync(gws, st));
     if (launches) *launches += 1;
 }
 
@@ -576,7 +605,7 @@ void thresh_csc(int64_t nrows_total, int64_t row0, int64_t nnz, int64_t ncols, c
                                                                cpos, crow);
         MSK_CHECK_LAUNCH();
     }
-    if (ncols) {
+    if (ncols && ccol) {
         k_csc_col<<<ceil_div_u(ncols, NT), NT, 0, st>>>(ncols, cptr, ccol);
         MSK_CHECK_LAUNCH();
     }

@@ -166,10 +166,16 @@ def test_patch_lagrange_matches_exact(msk, ctx, R, bar):
     h.close()
 
 
-def test_patch_too_large_is_invalid(msk, ctx):
+def test_patch_global_workspace_path(msk, ctx):
+    """A patch that does not fit in shared memory (R = 40: the whole coarse
+    levels) runs from a global workspace; with the patch covering the level the
+    result is the exact Lagrange function."""
     H = config("C3P4", m_eval=0)
     h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
-    with pytest.raises(msk.MskError) as ei:
-        h.assemble(T=3.0, lagrange_tol=1e-14, patch_R=40.0, patch_min_n=0)
-    assert ei.value.status == 1
+    h.assemble(T=3.0, lagrange_tol=1e-14)
+    ref = {(k, l): h.export_factor(k, l)[2] for k in range(1, H.L) for l in range(k)}
+    h.assemble(T=3.0, lagrange_tol=1e-14, patch_R=40.0, patch_min_n=0)
+    for (k, l), val in ref.items():
+        val2 = h.export_factor(k, l)[2]
+        assert np.abs(val2 - val).max() <= 1e-12 * np.abs(val).max(), (k, l)
     h.close()

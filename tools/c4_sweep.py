@@ -42,7 +42,7 @@ def main():
     base = {"config": args.config, "T": 0, "err_f_inf": float(np.abs(fe - s0).max())}
     print(json.dumps(base), flush=True)
     for T in range(1, args.Tmax + 1):
-        R = min(T + 8.0, 11.0)  # a larger patch (~940 points) exceeds one CTA's shared memory
+        R = T + 8.0  # patches beyond ~730 points run from a global workspace
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         h.assemble(T=float(T), lagrange_tol=1e-14, patch_R=R, patch_min_n=20000)
