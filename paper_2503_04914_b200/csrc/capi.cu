@@ -187,6 +187,16 @@ struct Timer {
     }
 };
 
+// On scope exit (also when an error unwinds the call), wait for the copy
+// streams: their transfers touch buffers that are freed on the compute stream.
+struct CopyStreamsGuard {
+    cudaStream_t a = nullptr, b = nullptr;
+    ~CopyStreamsGuard() {
+        if (a) cudaStreamSynchronize(a);
+        if (b) cudaStreamSynchronize(b);
+    }
+};
+
 // a synchronisation-only event
 struct Ev {
     cudaEvent_t e = nullptr;
@@ -1048,6 +1058,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         ad.emplace_back(alpha[l], (size_t)h->lev[l].n, st);
     }
     std::vector<Ev> ev_f((size_t)L), ev_a((size_t)L);
+    CopyStreamsGuard copy_guard{cin, cout};  // destroyed before fd / ad
     {
         Ev ready;
         ready.record(st);
@@ -1502,6 +1513,7 @@ void evaluate_pipelined(msk_hierarchy *h, int64_t m, const double *x, double *s,
     unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
     MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
     for (int l = 0; l < L; ++l) h->pack(l, h->lev[l].alpha, &launches);
+    CopyStreamsGuard copy_guard{cin, cout};
     Ev ready;
     ready.record(st);  // allocations (stream-ordered on st) before the copy streams touch them
     ready.wait_on(cin);
