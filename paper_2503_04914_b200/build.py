@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmsk.so")
-SOURCES = ["scan.cu", "celllist.cu", "assemble.cu", "gather.cu", "cg.cu", "thresh.cu", "misc.cu", "capi.cu"]
+SOURCES = ["scan.cu", "celllist.cu", "assemble.cu", "gather.cu", "cg.cu", "thresh.cu", "misc.cu", "capi.cu",
+           "capi_solve.cu", "capi_extra.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
