@@ -98,8 +98,15 @@ struct __align__(16) CGSharedTT {
     uint64_t bar_rp[2];
 };
 
+// ctr == nullptr: the group is one thread-block cluster (small levels, see
+// cg_batched) and the hardware cluster barrier (release / acquire at cluster
+// scope) replaces the counter in global memory.
 __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
                                               unsigned long long &round) {
+    if (ctr == nullptr) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
     __syncthreads();
     if (nb > 1) {
         round += (unsigned long long)nb;
@@ -1173,6 +1180,40 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
         poff += 3 * nch[l];
     }
     void *args[] = {&B};
+    // One small level (<= 16 chunks): a single thread-block cluster, one CTA per
+    // chunk, synchronised by the hardware cluster barrier instead of a counter in
+    // global memory (the iteration of a small level is latency bound): C3 levels
+    // 1/2 -10/-13 %, C2 levels 1/2 -16/-13 %.  With several chunks per CTA (64
+    // chunks on 16 CTAs) the cooperative launch is 2.3x faster, hence the bound.
+    // Same chunks, same partials, same order: bit-identical to the cooperative
+    // launch.  Falls back to it if the cluster cannot be scheduled.
+    if (nlev == 1 && nch[0] <= 16 && !getenv("MSK_NO_CLUSTER")) {
+        const int cl = (int)(nch[0] < 16 ? nch[0] : 16);
+        CGBatch C = B;
+        C.lev[0].nblocks = cl;
+        C.lev[0].barrier = nullptr;
+        void *cargs[] = {&C};
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cl);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = var.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaFuncSetAttribute(var.cg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (cudaLaunchKernelExC(&cfg, var.cg, cargs) == cudaSuccess) {
+            if (launches) *launches += 1;
+            MSK_CUDA(cudaFreeAsync(partials, st));
+            MSK_CUDA(cudaFreeAsync(bars, st));
+            return;
+        }
+        cudaGetLastError();  // clear, then the cooperative launch
+    }
     MSK_CUDA(cudaLaunchCooperativeKernel(var.cg, dim3(used), dim3(NT), args, var.smem, st));
     if (launches) *launches += 1;
     MSK_CUDA(cudaFreeAsync(partials, st));
