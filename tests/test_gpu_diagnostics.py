@@ -104,3 +104,13 @@ def test_figure3_nnz_ratio_matches_paper(msk, ctx, L):
         h.assemble(T=float(T), lagrange_tol=1e-14)
         assert _printed_eq(count(h) / den, want[T - 1], 5), (L, T)
     h.close()
+
+
+def test_m_diff_norm_needs_a_factor(msk, ctx):
+    H = grid_hierarchy(3)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    with pytest.raises(msk.MskError) as ei:
+        h.m_diff_norm()
+    assert ei.value.status == 6
+    h.close()
