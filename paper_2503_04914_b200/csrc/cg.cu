@@ -1092,11 +1092,15 @@ int cg_max_resident_blocks() {
     return r;
 }
 
-// tiles per chunk: a function of n only (keeps results launch-independent);
-// large levels use larger chunks to bound the partial-sum traffic
+// tiles per chunk: a function of n only (keeps results launch-independent,
+// and the same for the single-GPU, partitioned and multi-RHS paths).  Larger
+// chunks amortise the per-chunk work (row-pointer copy, partial reduction):
+// 4 tiles from 1024 tiles up, 2 from 512 (same-box A/B: C3 level 4 -18 %,
+// level 3 -7 %, C2 levels 4-5 -13/-7 %; 2 tiles at 256 tiles would halve the
+// CTAs of C2 level 3 and cost 28 %).
 int cg_chunk_tiles(int64_t n) {
     int64_t tiles = (n + NT - 1) / NT;
-    return tiles >= 16384 ? 4 : 1;
+    return tiles >= 1024 ? 4 : tiles >= 512 ? 2 : 1;
 }
 
 // levels[i].nblocks == 0 => the launcher assigns CTAs proportionally to work.

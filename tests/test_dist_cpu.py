@@ -123,5 +123,6 @@ def test_partition_rows_properties():
         for world in (1, 2, 3, 8):
             b = msk.msk_partition_rows(n, world)
             assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
-            rpc = (4 if (n + 255) // 256 >= 16384 else 1) * 256
+            tiles = (n + 255) // 256
+            rpc = (4 if tiles >= 1024 else 2 if tiles >= 512 else 1) * 256
             assert all(x % rpc == 0 for x in b[:-1])
