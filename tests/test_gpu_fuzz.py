@@ -1,0 +1,74 @@
+"""Seeded random hierarchies (dimension, Wendland k, level count and sizes,
+support multiplier nu, point family incl. non-nested uniform levels, a
+translated and scaled domain) through the whole path against the oracle:
+alpha per level within the 1e-9 bar, s_L within the kernel-sum rounding bound,
+both schedules; patterns of every A_l bit-exact."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import Hierarchy, franke, halton
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def msk():
+    import paper_2503_04914_b200 as m
+    m.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(msk):
+    c = msk.Context(0)
+    yield c
+    c.close()
+
+
+def _random_hierarchy(seed):
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([2, 3]))
+    k = int(rng.integers(0, 3))
+    L = int(rng.integers(1, 5))
+    n0 = int(rng.integers(20, 200))
+    growth = 4 if d == 2 else 6
+    sizes = [int(n0 * growth ** l * rng.uniform(0.8, 1.2)) for l in range(L)]
+    nu = float(rng.uniform(2.0, 4.5) if d == 2 else rng.uniform(1.3, 2.2))
+    nested = bool(rng.integers(0, 2))
+    shift = rng.uniform(-3, 3, size=d)
+    scale = float(rng.uniform(0.5, 4.0))
+    if nested:
+        allp = halton(max(sizes), d)
+        pts = [allp[:n] for n in sizes]
+    else:  # independent uniform levels (C-17: nesting is not required)
+        pts = [rng.random((n, d)) for n in sizes]
+    pts = [np.ascontiguousarray(p * scale + shift) for p in pts]
+    delta = [nu * scale * (np.sqrt(d) / 2) * n ** (-1.0 / d) for n in sizes]
+    q = [0.5 * scale * n ** (-1.0 / d) for n in sizes]
+    H = Hierarchy(f"fuzz{seed}", d, k, pts, delta, q, None)
+    f = [franke((p - shift) / scale) for p in pts]
+    x = np.ascontiguousarray(rng.random((500, d)) * scale + shift)
+    return H, f, x
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_against_oracle(msk, ctx, seed):
+    H, f, x = _random_hierarchy(seed)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    for l in range(H.L):
+        rp, col, _ = h.export_block(l, l)
+        orp, ocol = oracle.pattern(H.points[l], H.points[l], H.delta[l], "grid")
+        assert np.array_equal(rp, orp) and np.array_equal(col, ocol), (seed, l)
+    ao, _, _ = oracle.sequential(H.points, H.delta, f, tol=1e-12, k=H.k, direct_max_n=0)
+    so = oracle.evaluate(H.points, H.delta, ao, x, k=H.k)
+    scale = oracle.evaluate(H.points, H.delta, [np.abs(a) for a in ao], x, k=H.k)
+    for schedule in ("pruned", "literal"):
+        a, info = h.solve(f, tol=1e-12, schedule=schedule)
+        for l in range(H.L):
+            assert np.linalg.norm(a[l] - ao[l]) <= 1e-9 * np.linalg.norm(ao[l]) + 1e-300, (seed, schedule, l)
+        s, _ = h.evaluate(x)
+        # same coefficients to 1e-9 => values to 1e-9 of the absolute kernel sum
+        assert np.all(np.abs(s - so) <= 1e-9 * scale + 1e-300), (seed, schedule)
+    h.close()
