@@ -26,13 +26,13 @@ def ctx(msk):
     c.close()
 
 
-def _random_hierarchy(seed):
+def _random_hierarchy(seed, small=False):
     rng = np.random.default_rng(1000 + seed)
     d = int(rng.choice([2, 3]))
     k = int(rng.integers(0, 3))
-    L = int(rng.integers(1, 5))
-    n0 = int(rng.integers(20, 200))
-    growth = 4 if d == 2 else 6
+    L = int(rng.integers(2, 4)) if small else int(rng.integers(1, 5))
+    n0 = int(rng.integers(20, 60)) if small else int(rng.integers(20, 200))
+    growth = (3 if d == 2 else 4) if small else (4 if d == 2 else 6)
     sizes = [int(n0 * growth ** l * rng.uniform(0.8, 1.2)) for l in range(L)]
     nu = float(rng.uniform(2.0, 4.5) if d == 2 else rng.uniform(1.3, 2.2))
     nested = bool(rng.integers(0, 2))
@@ -71,4 +71,21 @@ def test_fuzz_against_oracle(msk, ctx, seed):
         s, _ = h.evaluate(x)
         # same coefficients to 1e-9 => values to 1e-9 of the absolute kernel sum
         assert np.all(np.abs(s - so) <= 1e-9 * scale + 1e-300), (seed, schedule)
+    h.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_thresholded_against_oracle(msk, ctx, seed):
+    """The thresholded path (a6/a7) on random small hierarchies (2-3 levels):
+    the factor's nonzero count equals the oracle's geometric count and alpha is
+    within the bar (exact Lagrange build)."""
+    H, f, x = _random_hierarchy(100 + seed, small=True)
+    T = float(np.random.default_rng(seed).choice([1.5, 2.0, 3.0, 5.0]))
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble(T=T, lagrange_tol=1e-14)
+    a, info = h.solve(f, tol=1e-12)
+    ao, _, nnz = oracle.thresholded(H.points, H.delta, H.q, T, f, k=H.k)
+    assert info.nnz_gather == nnz
+    for l in range(H.L):
+        assert np.linalg.norm(a[l] - ao[l]) <= 1e-9 * np.linalg.norm(ao[l]) + 1e-300, (seed, T, l)
     h.close()
