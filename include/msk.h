@@ -183,7 +183,7 @@ MSK_API msk_status msk_halo_plan(int world, int rank, const int64_t *rows, const
  *                NULL: computed exactly as 1/2 min distance when the
  *                closest pair lies within delta_l, else reported as delta_l/2.
  *   wendland_k   0, 1 or 2: phi_{d,k} (reading C-3).
- *   flags        MSK_FLAG_NONE.
+ *   flags        MSK_FLAG_NONE, or an OR of MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE.
  * Duplicate points within one level => MSK_ERR_INVALID. */
 MSK_API msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int64_t *n,
                                 const double *const *points, const double *delta,

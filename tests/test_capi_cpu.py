@@ -79,3 +79,26 @@ def test_fails_loudly_without_gpu(lib):
         m.Context(0)
     assert ei.value.status in (1, 3)
     assert m.msk_version().startswith("libmsk")
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2503_04914_b200")
+    exe = str(tmp_path / "msk_example")
+    subprocess.check_call(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror",
+                           os.path.join(root, "examples", "msk_example.c"), "-I", os.path.join(root, "include"),
+                           "-L", libdir, "-lmsk", f"-Wl,-rpath,{libdir}", "-lm", "-o", exe])
+    return exe
+
+
+def test_c_example_builds_and_fails_loudly_without_gpu(tmp_path):
+    """include/msk.h is plain C99 and libmsk links from C; without a usable
+    device the first call reports MSK_ERR_CUDA (no CPU path)."""
+    import subprocess
+    import torch
+    exe = _build_c_example(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present (tests/test_gpu_parity.py runs the example)")
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 2 and "msk_ctx_create" in r.stderr

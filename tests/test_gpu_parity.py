@@ -339,3 +339,21 @@ def test_edge_cases(msk, ctx):
         msk.Hierarchy(ctx, [np.zeros((3, 4))], [0.1])
     with pytest.raises(msk.MskError):
         h.solve(H.f(), tol=1.5)
+
+
+def test_c_example_runs(tmp_path):
+    """The C-ABI from plain C (examples/msk_example.c): host buffers, the
+    interpolation property s_L = f on X_L within 1e-10."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2503_04914_b200")
+    exe = str(tmp_path / "msk_example")
+    subprocess.check_call(["gcc", "-std=c99", "-O2", os.path.join(root, "examples", "msk_example.c"),
+                           "-I", os.path.join(root, "include"), "-L", libdir, "-lmsk",
+                           f"-Wl,-rpath,{libdir}", "-lm", "-o", exe])
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout)
+    assert out["points"] == [9, 25, 81] and out["max_interpolation_error"] < 1e-10
