@@ -209,6 +209,16 @@ MSK_API msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_
  * Non-convergence of a Lagrange solve => MSK_ERR_NOCONV. */
 MSK_API msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol);
 
+/* The T sweep of one factor build: every stored entry keeps
+ * the smallest integer t with ||x_j - x_i||^2 < (t q_l)^2 (reading C-5 recipe),
+ * so a factor built at T also serves every integer T' in [1, floor(T)] (at
+ * most 24): msk_set_threshold(h, T') makes msk_solve, msk_m_norm_ex and
+ * msk_export_factor use exactly the entries a fresh msk_assemble(T') would
+ * store, with the same values (the Lagrange functions do not depend on T) and
+ * in the same order -- bit-identical results.  T' == the build's T restores all
+ * entries.  MSK_ERR_STATE without a factor, MSK_ERR_INVALID for another T'. */
+MSK_API msk_status msk_set_threshold(msk_hierarchy *h, double T);
+
 /* msk_assemble with local-patch Lagrange functions for
  * the coarse levels with more than patch_min_n points (patch_R > 0): the
  * coefficients of chi_i^(l) solve A_l restricted to the patch

@@ -103,6 +103,10 @@ def msk_assemble(h, T=0.0, lagrange_tol=1e-13):
     check(load().msk_assemble(h, float(T), float(lagrange_tol)))
 
 
+def msk_set_threshold(h, T):
+    check(load().msk_set_threshold(h, float(T)))
+
+
 def msk_assemble_ex(h, T, lagrange_tol, patch_R, patch_min_n):
     check(load().msk_assemble_ex(h, float(T), float(lagrange_tol), float(patch_R), int(patch_min_n)))
 
@@ -307,6 +311,11 @@ class Hierarchy:
         info = msk_solve(self.handle, f, tol, max_iter, sch, alpha)
         self.last_solve = info
         return alpha, info
+
+    def set_threshold(self, T: float):
+        """Use the entries of the stored factor within T q_l (T integer <= the
+        build's T, or the build's T): the T sweep of one build."""
+        msk_set_threshold(self.handle, T)
 
     def solve_multi(self, F, tol=1e-12, max_iter=20000):
         """F: per level an (n_l, nrhs) array (numpy or CUDA tensor).  Returns

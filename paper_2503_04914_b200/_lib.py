@@ -77,6 +77,7 @@ def load() -> ctypes.CDLL:
         "msk_hierarchy_info_get": ([_vp, ctypes.POINTER(HierarchyInfo)], ctypes.c_int),
         "msk_assemble": ([_vp, _dbl, _dbl], ctypes.c_int),
         "msk_assemble_ex": ([_vp, _dbl, _dbl, _dbl, _i64], ctypes.c_int),
+        "msk_set_threshold": ([_vp, _dbl], ctypes.c_int),
         "msk_solve": ([_vp, pp, _dbl, _i32, ctypes.c_uint32, pp, ctypes.POINTER(SolveInfo)], ctypes.c_int),
         "msk_evaluate": ([_vp, _i64, _vp, _vp], ctypes.c_int),
         "msk_evaluate_ex": ([_vp, _i64, _vp, _vp, ctypes.POINTER(EvalInfo)], ctypes.c_int),
@@ -106,7 +107,7 @@ def load() -> ctypes.CDLL:
 
 
 EXPORTED = ["msk_ctx_create", "msk_ctx_destroy", "msk_hierarchy_create", "msk_hierarchy_destroy",
-            "msk_hierarchy_info_get", "msk_assemble", "msk_assemble_ex", "msk_solve", "msk_evaluate", "msk_evaluate_ex",
+            "msk_hierarchy_info_get", "msk_assemble", "msk_assemble_ex", "msk_set_threshold", "msk_solve", "msk_evaluate", "msk_evaluate_ex",
             "msk_solve_multi", "msk_evaluate_multi", "msk_m_norm", "msk_m_norm_ex",
             "msk_export_block", "msk_export_factor", "msk_export_cells", "msk_apply_block", "msk_cg_level",
             "msk_nccl_unique_id", "msk_partition_rows", "msk_halo_plan", "msk_last_error", "msk_version"]

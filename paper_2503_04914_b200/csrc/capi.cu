@@ -292,10 +292,15 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
         a.nt = h->lev[k].n;
         for (int q = 0; q < d; ++q) a.tx[q] = h->lev[k].xs + (size_t)q * h->lev[k].n;
         a.nlev = k;
+        a.nb = (int)std::min<double>(floor(T), (double)kMaxTBucket);
         for (int l = 0; l < k; ++l) {
             a.lev[l] = h->view(l);
             const double R = T * h->lev[l].q;
             a.R2[l] = R * R;
+            for (int t = 1; t <= a.nb; ++t) {  // the R2 recipe at integer T = t (reading C-5)
+                const double Rt = (double)t * h->lev[l].q;
+                a.tq2[l][t - 1] = Rt * Rt;
+            }
             a.reach[l] = (int)std::min(floor(R * h->lev[l].g.inv_cell) + 1.0, 1e6);
             a.col_off[l] = h->off[l];
         }
@@ -315,10 +320,12 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     h->tnnz = nnz;
     h->tcol = dalloc<int32_t>((size_t)nnz, st);
     h->tval = dalloc<double>((size_t)nnz, st);
+    h->tbucket = dalloc<uint8_t>((size_t)nnz, st);
     for (int k = 1; k < L; ++k) {
         ThreshPatternArgs a = pattern_args(k);
         a.row_ptr = h->trow_ptr + h->off[k];
         a.col = h->tcol;
+        a.bucket = h->tbucket;
         thresh_fill(a, st, launches);
     }
     // ---- transpose index over the coarse columns (levels 0..L-2)
@@ -443,6 +450,9 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     h->lagrange_max_iters = std::max(hstat[1], hps[2]);
     h->patch_max_points = hps[3];
     h->T = T;
+    h->T_active = T;
+    h->tmax_active = 255;
+    h->tnnz_active = h->tnnz;
     if (hstat[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: Lagrange CG did not converge in 20000 iterations");
     if (hps[1]) throw Error(MSK_ERR_INVALID, "msk_assemble: local patch overflow in " + std::to_string(hps[1]) +
                                                  " columns; reduce patch_R");
@@ -598,6 +608,21 @@ extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_t
     return msk_assemble_ex(h, T, lagrange_tol, 0.0, 0);
 }
 
+extern "C" msk_status msk_set_threshold(msk_hierarchy *h, double T) {
+    API_BEGIN
+    require(h != nullptr, "msk_set_threshold: NULL hierarchy");
+    if (!(h->T > 0.0)) throw Error(MSK_ERR_STATE, "msk_set_threshold: no thresholded factor (msk_assemble with T > 0)");
+    const int nb = (int)std::min<double>(floor(h->T), (double)kMaxTBucket);
+    const bool all = T == h->T;
+    require(all || (T == floor(T) && T >= 1.0 && T <= (double)nb),
+            "msk_set_threshold: T must equal the build's T or be an integer in [1, floor(build T)] (<= 24)");
+    MSK_CUDA(cudaSetDevice(h->ctx->device));
+    h->tmax_active = all ? 255 : (int)T;
+    h->T_active = T;
+    h->tnnz_active = all ? h->tnnz : bucket_count(h->tbucket, h->tnnz, h->tmax_active, h->st());
+    API_END
+}
+
 // ===================================================== row-level entry points
 extern "C" msk_status msk_export_block(msk_hierarchy *h, int row_level, int col_level,
                                        int64_t *row_ptr, int32_t *col, double *val) {
@@ -680,9 +705,11 @@ extern "C" msk_status msk_export_factor(msk_hierarchy *h, int row_level, int col
     const int64_t p0 = hrp[0], np = hrp[nr] - hrp[0];
     std::vector<int32_t> hcl((size_t)np), rperm((size_t)nr), cperm((size_t)C.n);
     std::vector<double> hvl((size_t)np);
+    std::vector<uint8_t> hbk((size_t)np);
     if (np) {
         MSK_CUDA(cudaMemcpyAsync(hcl.data(), h->tcol + p0, sizeof(int32_t) * np, cudaMemcpyDeviceToHost, st));
         MSK_CUDA(cudaMemcpyAsync(hvl.data(), h->tval + p0, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+        MSK_CUDA(cudaMemcpyAsync(hbk.data(), h->tbucket + p0, np, cudaMemcpyDeviceToHost, st));
     }
     MSK_CUDA(cudaMemcpyAsync(rperm.data(), R.perm, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaMemcpyAsync(cperm.data(), C.perm, sizeof(int32_t) * C.n, cudaMemcpyDeviceToHost, st));
@@ -697,7 +724,8 @@ extern "C" msk_status msk_export_factor(msk_hierarchy *h, int row_level, int col
         const int64_t i = inv[j];
         tmp.clear();
         for (int64_t p = hrp[i] - p0; p < hrp[i + 1] - p0; ++p)
-            if (hcl[p] >= c_lo && hcl[p] < c_hi) tmp.emplace_back(cperm[hcl[p] - c_lo], hvl[p]);
+            if (hcl[p] >= c_lo && hcl[p] < c_hi && hbk[p] <= h->tmax_active)
+                tmp.emplace_back(cperm[hcl[p] - c_lo], hvl[p]);
         std::sort(tmp.begin(), tmp.end());
         for (auto &e : tmp) {
             if (col) col[pos] = e.first;
@@ -706,7 +734,7 @@ extern "C" msk_status msk_export_factor(msk_hierarchy *h, int row_level, int col
         }
     }
     row_ptr[nr] = pos;
-    if (T_out) *T_out = h->T;
+    if (T_out) *T_out = h->T_active;
     API_END
 }
 

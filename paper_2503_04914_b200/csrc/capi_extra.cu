@@ -285,7 +285,8 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
         if (which == 1) {  // u += X~ v  (thresh_residual: out = base - sum val * (-v))
             MSK_CUDA(cudaMemcpyAsync(nv, v, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, st));
             dev_scale(nv, -1.0, N, st);
-            thresh_residual(h->off[1], N, h->trow_ptr, h->tcol, h->tval, u, nv, u, st, nullptr);
+            thresh_residual(h->off[1], N, h->trow_ptr, h->tcol, h->tval, u, nv, u, st, nullptr, h->tbucket,
+                            h->tmax_active);
         }
         const double s_new = sqrt(dev_dot(u, u, N, scratch, st));
         // w = M^T u = -A^{-1} (B^T u) on the coarse levels, 0 on the finest
@@ -311,7 +312,8 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
         }
         solve_coarse(t, w);
         MSK_CUDA(cudaMemsetAsync(w + h->off[L - 1], 0, sizeof(double) * (size_t)h->lev[L - 1].n, st));
-        if (which == 1) csc_spmv_add(ncols, cptr, cpos, crow, h->tval, u, w, st);  // w += X~^T u
+        if (which == 1)  // w += X~^T u
+            csc_spmv_add(ncols, cptr, cpos, crow, h->tval, u, w, st, h->tbucket, h->tmax_active);
         const double wn = sqrt(dev_dot(w, w, N, scratch, st));
         const bool done = it > 0 && fabs(s_new - sigma) <= rel_tol * s_new;
         sigma = s_new;

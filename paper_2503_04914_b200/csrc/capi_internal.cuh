@@ -249,6 +249,12 @@ struct msk_hierarchy {
     // are empty), global level-major spatial column indices
     double T = 0.0;
     int64_t tnnz = 0;
+    // T sweep (msk_set_threshold): per-entry distance bucket (smallest integer t with
+    // r^2 < (t q_l)^2); entries with bucket > tmax_active are left out
+    uint8_t *tbucket = nullptr;
+    int tmax_active = 255;
+    double T_active = 0.0;
+    int64_t tnnz_active = 0;
     int64_t *trow_ptr = nullptr;
     int32_t *tcol = nullptr;
     double *tval = nullptr;
@@ -284,10 +290,13 @@ struct msk_hierarchy {
 
     void release_factor() {
         cudaStream_t s = st();
-        dfree(trow_ptr, s); dfree(tcol, s); dfree(tval, s);
-        trow_ptr = nullptr; tcol = nullptr; tval = nullptr;
+        dfree(trow_ptr, s); dfree(tcol, s); dfree(tval, s); dfree(tbucket, s);
+        trow_ptr = nullptr; tcol = nullptr; tval = nullptr; tbucket = nullptr;
         tnnz = 0;
         T = 0.0;
+        T_active = 0.0;
+        tmax_active = 255;
+        tnnz_active = 0;
     }
 
     cudaStream_t st() const { return ctx->stream; }

@@ -390,7 +390,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             time_ga();
             for (int k = 1; k < L; ++k)
                 thresh_residual(h->off[k], h->off[k + 1], h->trow_ptr, h->tcol, h->tval, beta, beta, beta, st,
-                                &launches);
+                                &launches, h->tbucket, h->tmax_active);
             ga_t.back()->stop();
         } else {
             double *cur = h->ws_beta(0), *nxt = h->ws_t(0);
@@ -398,7 +398,8 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             MSK_CUDA(cudaMemcpyAsync(nxt, fsp, sizeof(double) * h->ntot, cudaMemcpyDeviceToDevice, st));
             time_ga();
             for (int sweep = 0; sweep < L; ++sweep) {
-                thresh_residual(h->off[1], h->ntot, h->trow_ptr, h->tcol, h->tval, fsp, cur, nxt, st, &launches);
+                thresh_residual(h->off[1], h->ntot, h->trow_ptr, h->tcol, h->tval, fsp, cur, nxt, st, &launches,
+                                h->tbucket, h->tmax_active);
                 std::swap(cur, nxt);
             }
             ga_t.back()->stop();
@@ -506,7 +507,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     loc.L = L;
     loc.jacobi_sweeps = schedule == MSK_SCHED_LITERAL ? L : 0;
     const int fin = schedule == MSK_SCHED_LITERAL && !thresholded ? L : 0;  // slot of the final solves
-    if (thresholded) hits = (unsigned long long)(h->tnnz * (schedule == MSK_SCHED_LITERAL ? L : 1));
+    if (thresholded) hits = (unsigned long long)(h->tnnz_active * (schedule == MSK_SCHED_LITERAL ? L : 1));
     std::string noconv;
     for (int s = 0; s < (thresholded ? 1 : nslots); ++s)
         for (int l = 0; l < L; ++l) {

@@ -198,6 +198,7 @@ void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
               const double *v, double *y, cudaStream_t st, int *launches);
 
 // ---- thresh.cu  (a6 / a7 thresholded factor)
+constexpr int kMaxTBucket = 24;
 struct ThreshPatternArgs {
     int d;
     int64_t nt;                     // target rows (points of one finer level, spatial order)
@@ -210,6 +211,11 @@ struct ThreshPatternArgs {
     const int64_t *row_ptr;         // fill: row pointers of these rows
     int32_t *cnt;                   // count: output
     int32_t *col;                   // fill: output (global columns)
+    // fill: distance bucket of each entry, the smallest integer t in 1..nb with
+    // r^2 < (t q_l)^2 (tq2[l][t-1], same rounding recipe as R2), else nb + 1
+    uint8_t *bucket;
+    int nb;
+    double tq2[kMaxLevels][kMaxTBucket];
 };
 void thresh_count(const ThreshPatternArgs &a, cudaStream_t st, int *launches);
 void thresh_fill(const ThreshPatternArgs &a, cudaStream_t st, int *launches);
@@ -280,10 +286,14 @@ void patch_count(const PatchArgs &a, int *pmax_out, cudaStream_t st);
 void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launches);
 size_t patch_smem_bytes(int pmax, int nnzmax);
 // out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)
+// bucket/tmax (optional): only entries with bucket <= tmax take part (the T sweep)
 void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,
-                  const double *u, double *out, cudaStream_t st);
+                  const double *u, double *out, cudaStream_t st, const uint8_t *bucket = nullptr, int tmax = 255);
 void thresh_residual(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col, const double *val,
-                     const double *base, const double *v, double *out, cudaStream_t st, int *launches);
+                     const double *base, const double *v, double *out, cudaStream_t st, int *launches,
+                     const uint8_t *bucket = nullptr, int tmax = 255);
+// number of entries with bucket <= tmax (device count, host result)
+int64_t bucket_count(const uint8_t *bucket, int64_t nnz, int tmax, cudaStream_t st);
 
 // ---- misc.cu
 // mm[0..2] = ordered keys of per-axis minima (init ~0), mm[3..5] maxima (init 0)

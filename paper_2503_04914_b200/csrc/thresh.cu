@@ -65,7 +65,15 @@ __global__ void __launch_bounds__(NT) k_tfill(ThreshPatternArgs a) {
                 double y[3];
 #pragma unroll
                 for (int t = 0; t < D; ++t) y[t] = L.x[t][j];
-                if (dist2_nofma<D>(x, y) < R2) a.col[p++] = off + j;
+                const double r2 = dist2_nofma<D>(x, y);
+                if (r2 < R2) {
+                    if (a.bucket) {
+                        int t = 1;
+                        while (t <= a.nb && !(r2 < a.tq2[l][t - 1])) ++t;
+                        a.bucket[p] = (uint8_t)t;
+                    }
+                    a.col[p++] = off + j;
+                }
             }
         });
     }
@@ -212,23 +220,36 @@ __global__ void k_csc_col(int64_t ncols, const int64_t *__restrict__ cptr, int32
 // out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)
 __global__ void __launch_bounds__(NT) k_tresidual(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
                                                   const int32_t *__restrict__ col, const double *__restrict__ val,
-                                                  const double *base, const double *v, double *out) {
+                                                  const double *base, const double *v, double *out,
+                                                  const uint8_t *__restrict__ bucket, int tmax) {
     const int64_t g = r0 + (int64_t)blockIdx.x * NT + threadIdx.x;
     if (g >= r1) return;
     double s = 0.0;
-    for (int64_t p = row_ptr[g]; p < row_ptr[g + 1]; ++p) s += val[p] * v[col[p]];
+    for (int64_t p = row_ptr[g]; p < row_ptr[g + 1]; ++p)
+        if (!bucket || bucket[p] <= tmax) s += val[p] * v[col[p]];
     out[g] = base[g] - s;
+}
+
+__global__ void k_bucket_count(const uint8_t *__restrict__ b, int64_t n, int tmax, unsigned long long *out) {
+    __shared__ long long sm[NT / 32 + 1];
+    long long c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT)
+        c += b[i] <= tmax;
+    c = block_sum_ll<NT>(c, sm);
+    if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)c);
 }
 // out[c] += sum over column c's entries of val[cpos[k]] * u[crow[k]] (transposed SpMV)
 __global__ void __launch_bounds__(NT) k_csc_spmv_add(int64_t ncols, const int64_t *__restrict__ cptr,
                                                      const int64_t *__restrict__ cpos,
                                                      const int32_t *__restrict__ crow,
                                                      const double *__restrict__ val, const double *__restrict__ u,
-                                                     double *__restrict__ out) {
+                                                     double *__restrict__ out, const uint8_t *__restrict__ bucket,
+                                                     int tmax) {
     const int64_t c = (int64_t)blockIdx.x * NT + threadIdx.x;
     if (c >= ncols) return;
     double s = 0.0;
-    for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k) s = fma(val[cpos[k]], u[crow[k]], s);
+    for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k)
+        if (!bucket || bucket[cpos[k]] <= tmax) s = fma(val[cpos[k]], u[crow[k]], s);
     out[c] += s;
 }
 
@@ -566,10 +587,25 @@ void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launc
 }
 
 void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,
-                  const double *u, double *out, cudaStream_t st) {
+                  const double *u, double *out, cudaStream_t st, const uint8_t *bucket, int tmax) {
     if (ncols <= 0) return;
-    k_csc_spmv_add<<<ceil_div_u(ncols, NT), NT, 0, st>>>(ncols, cptr, cpos, crow, val, u, out);
+    k_csc_spmv_add<<<ceil_div_u(ncols, NT), NT, 0, st>>>(ncols, cptr, cpos, crow, val, u, out, bucket, tmax);
     MSK_CHECK_LAUNCH();
+}
+
+int64_t bucket_count(const uint8_t *bucket, int64_t nnz, int tmax, cudaStream_t st) {
+    unsigned long long *d = nullptr, h = 0;
+    MSK_CUDA(cudaMallocAsync((void **)&d, sizeof(unsigned long long), st));
+    MSK_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+    if (nnz > 0) {
+        const int64_t nb = (nnz + NT - 1) / NT;
+        k_bucket_count<<<(unsigned)(nb < 1184 ? nb : 1184), NT, 0, st>>>(bucket, nnz, tmax, d);
+        MSK_CHECK_LAUNCH();
+    }
+    MSK_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    MSK_CUDA(cudaFreeAsync(d, st));
+    return (int64_t)h;
 }
 
 void thresh_count(const ThreshPatternArgs &a, cudaStream_t st, int *launches) {
@@ -635,9 +671,10 @@ void thresh_values(const ThreshValueArgs &a, cudaStream_t st, int *launches) {
 }
 
 void thresh_residual(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col, const double *val,
-                     const double *base, const double *v, double *out, cudaStream_t st, int *launches) {
+                     const double *base, const double *v, double *out, cudaStream_t st, int *launches,
+                     const uint8_t *bucket, int tmax) {
     if (r1 <= r0) return;
-    k_tresidual<<<ceil_div_u(r1 - r0, NT), NT, 0, st>>>(r0, r1, row_ptr, col, val, base, v, out);
+    k_tresidual<<<ceil_div_u(r1 - r0, NT), NT, 0, st>>>(r0, r1, row_ptr, col, val, base, v, out, bucket, tmax);
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
 }

@@ -106,6 +106,31 @@ def test_figure3_nnz_ratio_matches_paper(msk, ctx, L):
     h.close()
 
 
+@pytest.mark.parametrize("L", [5, 6])
+def test_figures_2_3_from_one_build(msk, ctx, L):
+    """Figures 2 and 3 from ONE factor build (T = 1e9, every entry of X) swept
+    with msk_set_threshold(T), T = 1..6: every printed digit of PAPER.md:
+    1365-1413 and 1439-1487, as with a build per T."""
+    H = grid_hierarchy(L)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    m, _ = h.m_norm(max_iter=2000, rel_tol=1e-11)
+    h.assemble(T=1e9, lagrange_tol=1e-14)
+
+    def count():
+        return sum(int(np.count_nonzero(np.abs(h.export_factor(k, l)[2]) > 1e-8))
+                   for k in range(1, L) for l in range(k))
+    den = count()
+    for T in range(1, 7):
+        h.set_threshold(float(T))
+        d, _ = h.m_diff_norm(max_iter=3000, rel_tol=1e-11)
+        assert _printed_eq(d / m, GOLDEN["figure2"][str(L)][T - 1], 5), (L, T, d / m)
+        assert _printed_eq(count() / den, GOLDEN["figure3"][str(L)][T - 1], 5), (L, T)
+    h.set_threshold(1e9)
+    assert count() == den
+    h.close()
+
+
 def test_m_diff_norm_needs_a_factor(msk, ctx):
     H = grid_hierarchy(3)
     h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)

@@ -179,3 +179,35 @@ def test_patch_global_workspace_path(msk, ctx):
         val2 = h.export_factor(k, l)[2]
         assert np.abs(val2 - val).max() <= 1e-12 * np.abs(val).max(), (k, l)
     h.close()
+
+
+# ------------------------------------------------------------------ T sweep
+@pytest.mark.parametrize("name", ["C1", "halton3d"])
+def test_threshold_sweep_equals_fresh_builds(msk, ctx, name):
+    """One build at T = 6 serves T' = 1..6 (msk_set_threshold): the same
+    entries, values and solve as a fresh build at T', bit for bit."""
+    H = HIERS[name]()
+    f = H.f()
+    fresh = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    sweep = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    sweep.assemble(T=6.0, lagrange_tol=LTOL)
+    for T in range(1, 7):
+        fresh.assemble(T=float(T), lagrange_tol=LTOL)
+        sweep.set_threshold(float(T))
+        for k in range(1, H.L):
+            for l in range(k):
+                a = fresh.export_factor(k, l)
+                b = sweep.export_factor(k, l)
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+                assert b[3] == T
+        af, i1 = fresh.solve(f, tol=1e-12)
+        asw, i2 = sweep.solve(f, tol=1e-12)
+        for l in range(H.L):
+            assert np.array_equal(af[l], asw[l]), (name, T, l)
+        assert i1.nnz_gather == i2.nnz_gather
+    sweep.set_threshold(6.0)
+    with pytest.raises(msk.MskError) as ei:
+        sweep.set_threshold(2.5)
+    assert ei.value.status == 1
+    fresh.close()
+    sweep.close()
