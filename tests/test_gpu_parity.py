@@ -151,8 +151,10 @@ def test_cg_level(msk, ctx, name):
         rp, col, val = oracle.block(H.points[l], H.points[l], H.delta[l], k=H.k)
         xo, ito, st = oracle.cg(rp, col, val, b, TOL)
         assert st == 0 and abs(it - ito) <= 2 and rr <= TOL
-        xd = oracle.cholesky_solve(rp, col, val, b)
-        assert _rel(x, xd) < BAR and _rel(xo, xd) < BAR
+        assert _rel(x, xo) < BAR
+        if len(H.points[l]) <= 5000:  # the oracle's dense Cholesky is O(n^3) in plain C (n = 9999: ~160 s)
+            xd = oracle.cholesky_solve(rp, col, val, b)
+            assert _rel(x, xd) < BAR and _rel(xo, xd) < BAR
         # the returned x satisfies the stopping rule on the true residual
         assert np.linalg.norm(oracle.spmv(rp, col, val, x) - b) <= 10 * TOL * np.linalg.norm(b)
 
