@@ -182,8 +182,8 @@ def test_patch_global_workspace_path(msk, ctx):
 
 
 # ------------------------------------------------------------------ T sweep
-@pytest.mark.parametrize("name", ["C1", "halton3d"])
-def test_threshold_sweep_equals_fresh_builds(msk, ctx, name):
+@pytest.mark.parametrize("name,schedule", [("C1", "pruned"), ("halton3d", "pruned"), ("C1", "literal")])
+def test_threshold_sweep_equals_fresh_builds(msk, ctx, name, schedule):
     """One build at T = 6 serves T' = 1..6 (msk_set_threshold): the same
     entries, values and solve as a fresh build at T', bit for bit."""
     H = HIERS[name]()
@@ -200,8 +200,8 @@ def test_threshold_sweep_equals_fresh_builds(msk, ctx, name):
                 b = sweep.export_factor(k, l)
                 assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
                 assert b[3] == T
-        af, i1 = fresh.solve(f, tol=1e-12)
-        asw, i2 = sweep.solve(f, tol=1e-12)
+        af, i1 = fresh.solve(f, tol=1e-12, schedule=schedule)
+        asw, i2 = sweep.solve(f, tol=1e-12, schedule=schedule)
         for l in range(H.L):
             assert np.array_equal(af[l], asw[l]), (name, T, l)
         assert i1.nnz_gather == i2.nnz_gather
