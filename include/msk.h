@@ -205,7 +205,11 @@ MSK_API msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_
  *           A_l^{-1} e_i (eq:chi P:373-377) solved by CG to relative residual
  *           lagrange_tol in (0,1).  msk_solve then runs the Jacobi sweep with
  *           the stored factor (eq:perturbed_split P:865-869).  Cost grows
- *           like sum_l N(l)^2 (one solve per coarse column).
+ *           like sum_l N(l)^2 (one solve per coarse column).  In a
+ *           distributed context the factor build is replicated on every rank
+ *           (the partitioned column levels keep their full A_l for it); the
+ *           Jacobi runs on the owned rows of the partitioned levels and their
+ *           CG is the partitioned CG (bit-identical to one GPU).
  * Non-convergence of a Lagrange solve => MSK_ERR_NOCONV. */
 MSK_API msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol);
 

@@ -470,7 +470,6 @@ extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrang
     require(std::isfinite(T), "msk_assemble: T must be finite");
     require(!(T > 0.0) || (lagrange_tol > 0.0 && lagrange_tol < 1.0),
             "msk_assemble: lagrange_tol must be in (0,1) when T > 0");
-    require(!(T > 0.0) || h->ctx->world == 1, "msk_assemble: the thresholded factor is single-GPU in this version");
     require(!(T > 0.0) || !(h->flags & MSK_FLAG_MATRIX_FREE),
             "msk_assemble: the thresholded factor needs assembled A_l (hierarchy is MSK_FLAG_MATRIX_FREE)");
     const bool mf = (h->flags & MSK_FLAG_MATRIX_FREE) != 0;
@@ -510,6 +509,7 @@ extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrang
         dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st);
         D.row_ptr = nullptr; D.col = nullptr; D.val = nullptr;
         nnz[l] = 0;
+        D.nnz = 0;  // (partitioned levels accumulate their partitions' entries below)
         if (h->dist[l].on) {  // owned rows only, per local partition
             for (auto &P : h->dist[l].local) {
                 const int64_t m = P.hi - P.lo;
@@ -518,7 +518,9 @@ extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrang
                 exclusive_scan_i64(D.cnt + P.lo, m, P.rp, st, &launches);
                 MSK_CUDA(cudaMemcpyAsync(&P.nnz, P.rp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             }
-            continue;
+            if (!(T > 0.0 && l + 1 < h->L)) continue;
+            // thresholded factor in a distributed context: the column levels keep
+            // their full A_l as well (the Lagrange build is replicated on every rank)
         }
         D.row_ptr = dalloc<int64_t>((size_t)(D.n + 3), st);  // + padding for 16-byte bulk copies
         MSK_CUDA(cudaMemsetAsync(D.row_ptr + D.n + 1, 0, 2 * sizeof(int64_t), st));
@@ -564,6 +566,14 @@ extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrang
                 D.nnz += P.nnz;
             }
             dfree(mm, st);
+            if (D.row_ptr) {  // full A_l of a column level (thresholded factor build)
+                D.col = dalloc<int32_t>((size_t)nnz[l] + 4, st);
+                D.val = dalloc<double>((size_t)nnz[l] + 2, st);
+                MSK_CUDA(cudaMemsetAsync(D.col + nnz[l], 0, 4 * sizeof(int32_t), st));
+                MSK_CUDA(cudaMemsetAsync(D.val + nnz[l], 0, 2 * sizeof(double), st));
+                LevelView v = h->view(l);
+                fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
+            }
             // every partition's halo range, known to all
             Dd.hlo.assign(W, 0);
             Dd.hhi.assign(W, 0);

@@ -197,7 +197,8 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     // ---- distributed solve of one partitioned level:
     // beta on the owned rows, then the CG as phase kernels with all-reduced
     // chunk partials and halo exchange of r; alpha assembled on every rank.
-    auto dist_level = [&](int l, double tl) {
+    // beta_ready: beta^(l) is already in ws_beta(l) (thresholded factor, a7)
+    auto dist_level = [&](int l, double tl, bool beta_ready) {
         auto &Dd = h->dist[l];
         LevelData &D = h->lev[l];
         const int64_t n = D.n;
@@ -231,7 +232,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             MSK_CUDA(cudaMemsetAsync(send[i], 0, sizeof(double) * (size_t)nch, st));
         }
         // beta^(l) on the owned rows (B products of the coarser, complete levels)
-        if (l > 0) {
+        if (l > 0 && !beta_ready) {
             for (auto &P : parts) {
                 GatherArgs ga{};
                 ga.d = h->d;
@@ -388,9 +389,29 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         if (schedule == MSK_SCHED_PRUNED) {
             MSK_CUDA(cudaMemcpyAsync(beta, fsp, sizeof(double) * h->ntot, cudaMemcpyDeviceToDevice, st));
             time_ga();
-            for (int k = 1; k < L; ++k)
-                thresh_residual(h->off[k], h->off[k + 1], h->trow_ptr, h->tcol, h->tval, beta, beta, beta, st,
-                                &launches, h->tbucket, h->tmax_active);
+            for (int k = 1; k < L; ++k) {
+                const auto &Dk = h->dist[k];
+                if (!Dk.on) {
+                    thresh_residual(h->off[k], h->off[k + 1], h->trow_ptr, h->tcol, h->tval, beta, beta, beta, st,
+                                    &launches, h->tbucket, h->tmax_active);
+                    continue;
+                }
+                // partitioned level: the owned rows, then beta^(k) complete on every
+                // rank for the finer levels' rows (zero-padded sum: exact)
+                for (const auto &P : Dk.local)
+                    thresh_residual(h->off[k] + P.lo, h->off[k] + P.hi, h->trow_ptr, h->tcol, h->tval, beta, beta,
+                                    beta, st, &launches, h->tbucket, h->tmax_active);
+                if (!h->ctx->emulated) {
+                    const int64_t nk = h->lev[k].n;
+                    const auto &P = Dk.local[0];
+                    double *tmp = h->ws_t(k);
+                    MSK_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * (size_t)nk, st));
+                    MSK_CUDA(cudaMemcpyAsync(tmp + P.lo, beta + h->off[k] + P.lo,
+                                             sizeof(double) * (size_t)(P.hi - P.lo), cudaMemcpyDeviceToDevice, st));
+                    MSK_NCCL(nccl_api()->AllReduce(tmp, beta + h->off[k], (size_t)nk, ncclFloat64, ncclSum,
+                                                   h->ctx->comm, st));
+                }
+            }
             ga_t.back()->stop();
         } else {
             double *cur = h->ws_beta(0), *nxt = h->ws_t(0);
@@ -407,13 +428,19 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         }
         std::vector<CGLevelArgs> a;
         for (int l = 0; l < L; ++l) {
+            if (h->dist[l].on) continue;  // partitioned levels: below
             a.push_back(cg_args(h, l, tol, max_iter, beta + h->off[l], nullptr, alpha_sp[l], ad[l].ptr,
                                 d_it + l, d_rr + 2 * l, d_stat + l));
             set_coef(a.back(), l);
         }
-        time_cg(-1);
-        cg_batched(a.data(), L, st, &launches);
-        cg_t.back()->stop();
+        if (!a.empty()) {
+            time_cg(-1);
+            cg_batched(a.data(), (int)a.size(), st, &launches);
+            cg_t.back()->stop();
+        }
+        // (distributed context) the partitioned levels: beta^(l) = ws_beta(l) from the Jacobi
+        for (int l = 0; l < L; ++l)
+            if (h->dist[l].on) dist_level(l, tol, true);
     } else if (schedule == MSK_SCHED_PRUNED) {
         // Algorithm 2 with every inner solve done once, when its input is final:
         // beta^(l) = f^(l) - sum_{k<l} B_lk t^(k); t^(l) = A_l^{-1} beta^(l);
@@ -423,7 +450,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             const double tl = l + 1 < L ? inner_tol : tol;
             wait_f(l);
             if (h->dist[l].on || mf) {
-                dist_level(l, tl);
+                dist_level(l, tl, false);
                 out_alpha(l);
                 debug_sync(st, "dist_level");
                 if (l + 1 < L) h->pack(l, alpha_sp[l], &launches);

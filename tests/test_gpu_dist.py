@@ -79,3 +79,35 @@ def test_partitioned_matches_oracle_and_default_threshold(msk):
         h.cg_level(3, f[3])
     assert ei.value.status == 6
     cw.close()
+
+
+@pytest.mark.parametrize("name,T", [("C1", 2.0), ("halton3d", 3.0), ("C3P4", 2.0)])
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_thresholded_equals_single_gpu_bitwise(msk, name, T, world):
+    """a6/a7 in a distributed context: the factor build is
+    replicated, the thresholded Jacobi runs on each partition's rows of the
+    partitioned levels and the CG of those levels is the partitioned CG; alpha,
+    iterations and the stored factor equal the single-GPU thresholded solve bit
+    for bit."""
+    H = HIERS[name]()
+    f = H.f()
+    res = []
+    for ctx, flags in ((msk.Context(0), 0), (msk.Context(0, rank=-1, world=world), msk.MSK_FLAG_DIST_ALL)):
+        h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=flags)
+        h.assemble(T=T, lagrange_tol=1e-14)
+        a, info = h.solve(f, tol=1e-12)
+        fac = [h.export_factor(k, l) for k in range(1, H.L) for l in range(k)]
+        # the T sweep works on the distributed factor as well
+        h.set_threshold(1.0)
+        a1, _ = h.solve(f, tol=1e-12)
+        res.append((a, info, fac, a1, h.info().nnz_A))
+        h.close()
+        ctx.close()
+    (a, i, fac, a1, nA), (aw, iw, facw, a1w, nAw) = res
+    for l in range(H.L):
+        assert np.array_equal(aw[l], a[l]), (name, world, l, np.abs(aw[l] - a[l]).max())
+        assert np.array_equal(a1w[l], a1[l])
+        assert iw.cg_iters[l] == i.cg_iters[l]
+    assert list(nAw) == list(nA)
+    for x, y in zip(fac, facw):
+        assert all(np.array_equal(u, v) for u, v in zip(x[:3], y[:3]))
