@@ -81,9 +81,10 @@ def test_partitioned_matches_oracle_and_default_threshold(msk):
     cw.close()
 
 
-@pytest.mark.parametrize("name,T", [("C1", 2.0), ("halton3d", 3.0), ("C3P4", 2.0)])
+@pytest.mark.parametrize("name,T,patch_R", [("C1", 2.0, 0.0), ("halton3d", 3.0, 0.0), ("C3P4", 2.0, 0.0),
+                                             ("halton3d", 3.0, 9.0)])
 @pytest.mark.parametrize("world", [2, 3])
-def test_partitioned_thresholded_equals_single_gpu_bitwise(msk, name, T, world):
+def test_partitioned_thresholded_equals_single_gpu_bitwise(msk, name, T, patch_R, world):
     """a6/a7 in a distributed context: the factor build is
     replicated, the thresholded Jacobi runs on each partition's rows of the
     partitioned levels and the CG of those levels is the partitioned CG; alpha,
@@ -94,7 +95,8 @@ def test_partitioned_thresholded_equals_single_gpu_bitwise(msk, name, T, world):
     res = []
     for ctx, flags in ((msk.Context(0), 0), (msk.Context(0, rank=-1, world=world), msk.MSK_FLAG_DIST_ALL)):
         h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=flags)
-        h.assemble(T=T, lagrange_tol=1e-14)
+        # patch_R > 0: local-patch Lagrange functions for the column levels above 1000 points
+        h.assemble(T=T, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=1000)
         a, info = h.solve(f, tol=1e-12)
         fac = [h.export_factor(k, l) for k in range(1, H.L) for l in range(k)]
         # the T sweep works on the distributed factor as well
