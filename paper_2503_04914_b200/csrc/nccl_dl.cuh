@@ -2,10 +2,16 @@
 // torch.distributed has already loaded into the process (dlopen RTLD_NOLOAD),
 // else from the system library.  libmsk has no link-time NCCL dependency, and
 // a process never carries two NCCL instances.
+//
+// MSK_NCCL_LIBRARY=<path> (test hook) resolves the entry points from that
+// library instead: tests/nccl_shim implements the same API in-process for
+// threads-as-ranks, so the rank >= 0 code path (halo plans, grouped
+// send/recv, all-reduce sequencing) runs on one GPU without NCCL itself.
 #pragma once
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -26,11 +32,14 @@ struct NcclApi {
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-inline NcclApi *nccl_api() {
-    static NcclApi api;
-    static bool loaded = false;
-    if (loaded) return &api;
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+inline NcclApi nccl_load() {
+    NcclApi api;
+    void *h = nullptr;
+    if (const char *lib = std::getenv("MSK_NCCL_LIBRARY")) {
+        h = dlopen(lib, RTLD_NOW | RTLD_LOCAL);
+        if (!h) throw Error(4, std::string("MSK_NCCL_LIBRARY: ") + dlerror());
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) throw Error(4, std::string("NCCL not available: ") + dlerror());
@@ -49,7 +58,13 @@ inline NcclApi *nccl_api() {
     api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
-    loaded = true;
+    return api;
+}
+
+// One resolution per process; thread-safe (ranks may be threads, see above).
+// A failed resolution throws and is retried by the next call.
+inline NcclApi *nccl_api() {
+    static NcclApi api = nccl_load();
     return &api;
 }
 

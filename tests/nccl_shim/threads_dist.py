@@ -1,0 +1,114 @@
+"""TEST INFRASTRUCTURE (run by tests/test_gpu_rank_threads.py in a subprocess).
+
+The rank >= 0 distributed path of libmsk -- one msk_ctx per rank created
+with an NCCL unique id, halo plans from all-gathered column ranges, grouped
+ncclSend/ncclRecv of r halos, zero-filled all-reduces -- run with `world`
+ranks as THREADS of this process on one GPU.  The NCCL entry points come from
+tests/nccl_shim (MSK_NCCL_LIBRARY, set by the caller before libmsk resolves
+NCCL), which checks that every rank issues the same collectives and that
+every receive matches a send.  Every rank's alpha, iteration counts and s_L
+must equal the single-GPU solve bit for bit, exact and
+thresholded (with the T sweep).
+
+Usage: python tests/nccl_shim/threads_dist.py WORLD
+Prints one line per case and "ALL OK" at the end; exits non-zero on failure.
+"""
+import ctypes
+import os
+import sys
+import threading
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from workloads import config, halton_hierarchy, uniform_points  # noqa: E402
+
+import paper_2503_04914_b200 as msk  # noqa: E402
+
+DIST_ALL = msk.MSK_FLAG_DIST_ALL
+CASES = [  # (name, hierarchy, T, patch_R, flags of the rank contexts' hierarchies)
+    ("C1", lambda: config("C1", m_eval=0), 0.0, 0.0, DIST_ALL),
+    ("halton3d", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 0.0, 0.0, DIST_ALL),
+    ("C3P4", lambda: config("C3P4", m_eval=0), 0.0, 0.0, DIST_ALL),
+    ("halton3d-T3", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 3.0, 0.0, DIST_ALL),
+    ("C3P4-T2", lambda: config("C3P4", m_eval=0), 2.0, 0.0, DIST_ALL),
+    ("halton3d-T3-patch", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 3.0, 9.0, DIST_ALL),
+    # bench.py's setting (no DIST_ALL): only the 1.25M-point level (>= 2^20) is partitioned
+    ("C3P5-default", lambda: config("C3P5", m_eval=0), 0.0, 0.0, 0),
+]
+
+
+def run(ctx, H, f, x, T, patch_R, flags):
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=flags)
+    h.assemble(T=T, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=1000)
+    a, info = h.solve(f, tol=1e-12)
+    out = {"alpha": a, "iters": list(info.cg_iters)[:H.L]}
+    if T > 0:
+        h.set_threshold(1.0)
+        out["alpha_T1"], _ = h.solve(f, tol=1e-12)
+    else:
+        out["s"], _ = h.evaluate(x)
+    h.close()
+    return out
+
+
+def shim_stats():
+    out = (ctypes.c_long * 5)()
+    ctypes.CDLL(os.environ["MSK_NCCL_LIBRARY"]).msk_shim_stats(out)
+    return dict(zip(("allreduce", "allgather", "send", "recv", "comm_init"), out))
+
+
+def main(world: int) -> None:
+    msk.load()
+    for name, mk, T, patch_R, flags in CASES:
+        H = mk()
+        f = H.f()
+        x = uniform_points(5000, H.d, seed=4)
+        c1 = msk.Context(0)
+        ref = run(c1, H, f, x, T, patch_R, 0)  # also initialises libmsk's per-process state
+        c1.close()
+        nid = msk.msk_nccl_unique_id()
+        res, err = [None] * world, [None] * world
+
+        def rank_main(r):
+            try:
+                ctx = msk.Context(0, None, r, world, nid)
+                res[r] = run(ctx, H, f, x, T, patch_R, flags)
+                ctx.close()
+            except BaseException as e:  # reported by the main thread
+                err[r] = e
+
+        th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+        s0 = shim_stats()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        s1 = {k: s1 - s0[k] for k, s1 in shim_stats().items()}
+        for r in range(world):
+            if err[r] is not None:
+                raise RuntimeError(f"{name}: rank {r} failed: {err[r]!r}")
+            got = res[r]
+            for l in range(H.L):
+                assert np.array_equal(got["alpha"][l], ref["alpha"][l]), \
+                    (name, r, l, float(np.abs(got["alpha"][l] - ref["alpha"][l]).max()))
+            assert got["iters"] == ref["iters"], (name, r, got["iters"], ref["iters"])
+            if T > 0:
+                for l in range(H.L):
+                    assert np.array_equal(got["alpha_T1"][l], ref["alpha_T1"][l]), (name, r, l, "T=1")
+            else:
+                assert np.array_equal(got["s"], ref["s"]), (name, r, "s_L")
+        # the transport really carried the solve: per-rank init, halos, reductions
+        assert s1["comm_init"] == world and s1["allgather"] > 0 and s1["allreduce"] > 0, s1
+        assert s1["send"] > 0 and s1["send"] == s1["recv"], s1
+        print(f"{name} world={world}: {world} ranks bit-identical to one GPU, iters {ref['iters']}, "
+              f"shim calls {s1}", flush=True)
+    print("ALL OK", flush=True)
+
+
+if __name__ == "__main__":
+    if not os.environ.get("MSK_NCCL_LIBRARY"):
+        sys.exit("set MSK_NCCL_LIBRARY to the built tests/nccl_shim library")
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
