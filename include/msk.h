@@ -61,7 +61,7 @@ typedef enum {
                              (q_l = 0 => A_l singular); tol not in (0,1); null pointer */
     MSK_ERR_NOMEM = 2,    /* device allocation failed */
     MSK_ERR_CUDA = 3,     /* CUDA runtime error (includes: no device) */
-    MSK_ERR_NCCL = 4,     /* reserved for the multi-GPU communicator */
+    MSK_ERR_NCCL = 4,     /* NCCL unavailable or an NCCL call failed (multi-GPU context) */
     MSK_ERR_NOCONV = 5,   /* CG reached max_iter; msk_last_error names level and residual */
     MSK_ERR_STATE = 6     /* call out of order (e.g. msk_solve before msk_assemble) */
 } msk_status;
@@ -140,7 +140,10 @@ typedef struct {
  *   world_size in 2..16, 0 <= rank < world_size, nccl_unique_id = the 128-byte
  *     ncclUniqueId from msk_nccl_unique_id on rank 0 (broadcast by the caller,
  *     e.g. with torch.distributed): one partition per rank over NCCL (the
- *     libnccl already loaded by the process is used);
+ *     libnccl already loaded by the process is used; the environment variable
+ *     MSK_NCCL_LIBRARY=<path> names another library exporting the same NCCL
+ *     entry points instead -- the tests' in-process shim for ranks that are
+ *     threads of one process, tests/nccl_shim);
  *   world_size in 2..16, rank == -1, nccl_unique_id NULL: single-process
  *     emulation -- all world_size partitions run on this device and exchange
  *     through device copies (used to test the partitioned path on one GPU).
