@@ -179,7 +179,8 @@ MSK_API msk_status msk_halo_plan(int world, int rank, const int64_t *rows, const
  * stably sorted by (cell key, original index)).
  *   d            2 or 3.
  *   L            1..16 levels, coarse to fine.
- *   n [host]     L point counts.
+ *   n [host]     L point counts, each in 1 .. 2^31 - 2 (an empty level has no
+ *                interpolant: MSK_ERR_INVALID).
  *   points       L pointers, each n[l] x d row-major FP64 (host or device).
  *   delta [host] L support radii delta_l > 0 (eq:deltadef P:105-107: nu h_l).
  *   q [host]     L separation values (used only by thresholding), or

@@ -339,6 +339,9 @@ def test_edge_cases(msk, ctx):
         msk.Hierarchy(ctx, [H.points[0]], [-1.0])
     with pytest.raises(msk.MskError):
         msk.Hierarchy(ctx, [np.zeros((3, 4))], [0.1])
+    with pytest.raises(msk.MskError) as ei:             # empty level
+        msk.Hierarchy(ctx, [H.points[0], np.zeros((0, 2))], [0.2, 0.1])
+    assert ei.value.status == 1
     with pytest.raises(msk.MskError):
         h.solve(H.f(), tol=1.5)
 
