@@ -10,7 +10,9 @@ every receive matches a send.  Every rank's alpha, iteration counts and s_L
 must equal the single-GPU solve bit for bit, exact and
 thresholded (with the T sweep).
 
-Usage: python tests/nccl_shim/threads_dist.py WORLD
+Usage: python tests/nccl_shim/threads_dist.py WORLD [--full]
+(--full: the bench configuration instead, C3 with 10^7 points on the finest
+level and 10^6 evaluation points, no DIST_ALL.)
 Prints one line per case and "ALL OK" at the end; exits non-zero on failure.
 """
 import ctypes
@@ -38,6 +40,7 @@ CASES = [  # (name, hierarchy, T, patch_R, flags of the rank contexts' hierarchi
     # bench.py's setting (no DIST_ALL): only the 1.25M-point level (>= 2^20) is partitioned
     ("C3P5-default", lambda: config("C3P5", m_eval=0), 0.0, 0.0, 0),
 ]
+FULL = [("C3-default", lambda: config("C3", m_eval=0), 0.0, 0.0, 0)]
 
 
 def run(ctx, H, f, x, T, patch_R, flags):
@@ -60,12 +63,12 @@ def shim_stats():
     return dict(zip(("allreduce", "allgather", "send", "recv", "comm_init"), out))
 
 
-def main(world: int) -> None:
+def main(world: int, full: bool = False) -> None:
     msk.load()
-    for name, mk, T, patch_R, flags in CASES:
+    for name, mk, T, patch_R, flags in (FULL if full else CASES):
         H = mk()
         f = H.f()
-        x = uniform_points(5000, H.d, seed=4)
+        x = uniform_points(10 ** 6 if full else 5000, H.d, seed=4)
         c1 = msk.Context(0)
         ref = run(c1, H, f, x, T, patch_R, 0)  # also initialises libmsk's per-process state
         c1.close()
@@ -111,4 +114,4 @@ def main(world: int) -> None:
 if __name__ == "__main__":
     if not os.environ.get("MSK_NCCL_LIBRARY"):
         sys.exit("set MSK_NCCL_LIBRARY to the built tests/nccl_shim library")
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 2, "--full" in sys.argv)

@@ -51,3 +51,15 @@ def test_rank_threads_equal_single_gpu_bitwise(world):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "nccl_shim", "threads_dist.py"), str(world)],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_rank_threads_full_size_bench_configuration():
+    """C3 as bench.py --gpus 2 runs it (levels >= 2^20 points partitioned:
+    the 1.25M and 10M levels), 10^6 evaluation points: both ranks bit-identical
+    to the single-GPU solve."""
+    lib = build_shim()
+    env = dict(os.environ, MSK_NCCL_LIBRARY=lib, MSK_SHIM_TIMEOUT_S="120")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "nccl_shim", "threads_dist.py"), "2", "--full"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
