@@ -1113,7 +1113,10 @@ void set_smem_attrs() {
 }
 
 // variant by mean row length (entries per row of the work being launched)
-int cg_variant(double nnz, double rows) { return rows > 0 && nnz >= 16.0 * rows ? 1 : 0; }
+#ifndef MSK_LONGROW
+#define MSK_LONGROW 16.0
+#endif
+int cg_variant(double nnz, double rows) { return rows > 0 && nnz >= MSK_LONGROW * rows ? 1 : 0; }
 }  // namespace
 
 int cg_max_resident_blocks() {
