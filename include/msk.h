@@ -184,8 +184,9 @@ MSK_API msk_status msk_halo_plan(int world, int rank, const int64_t *rows, const
  *   points       L pointers, each n[l] x d row-major FP64 (host or device).
  *   delta [host] L support radii delta_l > 0 (eq:deltadef P:105-107: nu h_l).
  *   q [host]     L separation values (used only by thresholding), or
- *                NULL: computed exactly as 1/2 min distance when the
- *                closest pair lies within delta_l, else reported as delta_l/2.
+ *                NULL: computed exactly as 1/2 min distance: from
+ *                the pattern pass when the closest pair lies within delta_l,
+ *                else by a widening cell search (a one-point level: delta_l/2).
  *   wendland_k   0, 1 or 2: phi_{d,k} (reading C-3).
  *   flags        MSK_FLAG_NONE, or an OR of MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE.
  * Duplicate points within one level => MSK_ERR_INVALID. */
@@ -235,8 +236,11 @@ MSK_API msk_status msk_set_threshold(msk_hierarchy *h, double T);
  * and one shared-memory system per column, so the build costs O(N(l)) instead
  * of O(N(l)^2).  An approximation of the exact factor: the error at the stored
  * entries falls with patch_R - T.  patch_R <= 0: exactly
- * msk_assemble.  A patch that does not fit in shared memory =>
- * MSK_ERR_INVALID (reduce patch_R). */
+ * msk_assemble.  A patch whose workspace does not fit in one CTA's shared
+ * memory runs from a per-CTA slice of a global workspace (slower: the vectors
+ * then live in L2); a patch workspace above 1 GiB => MSK_ERR_INVALID (reduce
+ * patch_R).  On any error the hierarchy is left unassembled (msk_solve =>
+ * MSK_ERR_STATE until the next successful msk_assemble). */
 MSK_API msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrange_tol, double patch_R,
                            int64_t patch_min_n);
 
@@ -329,6 +333,14 @@ MSK_API msk_status msk_export_factor(msk_hierarchy *h, int row_level, int col_le
  * Any output may be NULL. */
 MSK_API msk_status msk_export_cells(msk_hierarchy *h, int level, int32_t *perm, int32_t *cell_start,
                             int64_t *cell_key, double *lo, double *cell, int64_t *dims);
+
+/* The exact grid of level l (a1; reading C-26): origin lo [host] d doubles,
+ * inv_cell [host] 1 double -- the FP64 factor of the key map, so a point's
+ * cell coordinate along axis a is floor((x_a - lo_a) * inv_cell) with one
+ * rounded subtraction and one rounded multiplication (no FMA, reading C-4),
+ * clamped to [0, dims_a - 1] -- and dims [host] d int64.  Any output may be
+ * NULL.  MSK_ERR_INVALID for a bad level. */
+MSK_API msk_status msk_export_grid(msk_hierarchy *h, int level, double *lo, double *inv_cell, int64_t *dims);
 
 /* y = B_{row_level,col_level} v (a3).  row_level == col_level uses the
  * assembled A_l (CSR SpMV kernel; requires msk_assemble), row_level >

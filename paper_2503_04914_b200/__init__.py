@@ -174,6 +174,10 @@ def msk_export_cells(h, level, perm, cell_start, cell_key, lo, cell, dims):
                                   _ptr(cell), _ptr(dims)))
 
 
+def msk_export_grid(h, level, lo, inv_cell, dims):
+    check(load().msk_export_grid(h, level, _ptr(lo), _ptr(inv_cell), _ptr(dims)))
+
+
 def msk_apply_block(h, row_level, col_level, v, y):
     t = ctypes.c_double(0.0)
     check(load().msk_apply_block(h, row_level, col_level, _ptr(v), _ptr(y), ctypes.byref(t)))
@@ -392,8 +396,10 @@ class Hierarchy:
         cell = np.zeros(1)
         dims = np.zeros(3, dtype=np.int64)
         msk_export_cells(self.handle, level, perm, cs, keys, lo, cell, dims)
+        inv = np.zeros(1)
+        msk_export_grid(self.handle, level, None, inv, None)
         return dict(perm=perm, cell_start=cs, keys=keys, lo=lo[:self.d], cell=float(cell[0]),
-                    dims=dims[:self.d])
+                    inv_cell=float(inv[0]), dims=dims[:self.d])
 
     def apply_block(self, row_level: int, col_level: int, v, y=None):
         v = _f64(v)

@@ -87,6 +87,7 @@ def load() -> ctypes.CDLL:
         "msk_m_norm_ex": ([_vp, _i32, _i32, _dbl, _dbl, ctypes.POINTER(_dbl), ctypes.POINTER(_i32)], ctypes.c_int),
         "msk_export_block": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
         "msk_export_cells": ([_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+        "msk_export_grid": ([_vp, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
         "msk_export_factor": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(_dbl)],
                               ctypes.c_int),
         "msk_apply_block": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.POINTER(_dbl)], ctypes.c_int),
@@ -109,7 +110,7 @@ def load() -> ctypes.CDLL:
 EXPORTED = ["msk_ctx_create", "msk_ctx_destroy", "msk_hierarchy_create", "msk_hierarchy_destroy",
             "msk_hierarchy_info_get", "msk_assemble", "msk_assemble_ex", "msk_set_threshold", "msk_solve", "msk_evaluate", "msk_evaluate_ex",
             "msk_solve_multi", "msk_evaluate_multi", "msk_m_norm", "msk_m_norm_ex",
-            "msk_export_block", "msk_export_factor", "msk_export_cells", "msk_apply_block", "msk_cg_level",
+            "msk_export_block", "msk_export_factor", "msk_export_cells", "msk_export_grid", "msk_apply_block", "msk_cg_level",
             "msk_nccl_unique_id", "msk_partition_rows", "msk_halo_plan", "msk_last_error", "msk_version"]
 MSK_FLAG_DIST_ALL = 1
 MSK_FLAG_MATRIX_FREE = 2

@@ -4,6 +4,8 @@
 // the definition; candidates are screened by the conservative FP32 prefilter
 // first (for_each_hit, neighbors.cuh), which never drops a true neighbour.  Values Phi_delta(r) = delta^-d phi(r / delta)
 // (eq:kernelscaling P:67) with the column level's delta (reading C-1).
+#include <string.h>
+
 #include "kernels.cuh"
 #include "neighbors.cuh"
 
@@ -38,6 +40,37 @@ __global__ void __launch_bounds__(NT) k_count(LevelView rows, LevelView cols, in
         }
         if ((threadIdx.x & 31) == 0) atomicMin(min_r2_bits, bits);
     }
+}
+
+// Nearest pair of a level beyond its support (q = 1/2 min distance when no
+// pair lies within delta): every candidate within m cells per axis,
+// r^2 without FMA (reading C-4).  A pair closer than m cell sides is always
+// found, so the caller grows m until the minimum is below m cell sides.
+template <int D>
+__global__ void __launch_bounds__(NT) k_min_r2_reach(LevelView v, int m, unsigned long long *__restrict__ min_r2_bits) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    if (i < v.n) {
+        double x[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = v.x[a][i];
+        for_each_range_m<D>(v, x, m, [&](int b, int e) {
+            for (int j = b; j < e; ++j) {
+                if (j == i) continue;
+                double y[3];
+#pragma unroll
+                for (int a = 0; a < D; ++a) y[a] = v.x[a][j];
+                const double r2 = dist2_nofma<D>(x, y);
+                best = r2 < best ? r2 : best;
+            }
+        });
+    }
+    unsigned long long bits = (unsigned long long)__double_as_longlong(best);
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, bits, o);
+        bits = t < bits ? t : bits;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(min_r2_bits, bits);
 }
 
 template <int D, int K>
@@ -118,6 +151,24 @@ void fill_pattern(int d, int k, const LevelView &rows, const LevelView &cols,
 #undef MSK_FILL
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
+}
+
+// min r^2 over the pairs of level v whose cells differ by at most m per axis
+double min_r2_reach(int d, const LevelView &v, int m, cudaStream_t st) {
+    unsigned long long *dm = nullptr, hm = 0x7ff0000000000000ull;
+    MSK_CUDA(cudaMallocAsync((void **)&dm, sizeof hm, st));
+    MSK_CUDA(cudaMemcpyAsync(dm, &hm, sizeof hm, cudaMemcpyHostToDevice, st));
+    if (v.n > 0) {
+        if (d == 2) k_min_r2_reach<2><<<ceil_div_u(v.n, NT), NT, 0, st>>>(v, m, dm);
+        else k_min_r2_reach<3><<<ceil_div_u(v.n, NT), NT, 0, st>>>(v, m, dm);
+        MSK_CHECK_LAUNCH();
+    }
+    MSK_CUDA(cudaMemcpyAsync(&hm, dm, sizeof hm, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    MSK_CUDA(cudaFreeAsync(dm, st));
+    double r2;
+    memcpy(&r2, &hm, sizeof r2);
+    return r2;
 }
 
 }  // namespace msk

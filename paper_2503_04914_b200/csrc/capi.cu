@@ -175,17 +175,25 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
             h->off[l + 1] = h->off[l] + n[l];
             double cell = delta[l] * (1.0 + 0x1p-20);
             for (;;) {
-                Grid g{};
-                g.inv_cell = 1.0 / cell;
-                g.ncells = 1;
+                // the cell count is formed in double first: extent / delta can be
+                // large enough (3-D, > ~2.6e6 per axis) to overflow int64 products
+                double dims_d[3], ncells_d = 1.0;
                 for (int a = 0; a < 3; ++a) {
-                    g.lo[a] = a < d ? h->lo[a] : 0.0;
-                    g.dim[a] = a < d ? (int64_t)floor((h->hi[a] - h->lo[a]) * g.inv_cell) + 1 : 1;
-                    g.ncells *= g.dim[a];
+                    dims_d[a] = a < d ? floor((h->hi[a] - h->lo[a]) * (1.0 / cell)) + 1.0 : 1.0;
+                    ncells_d *= dims_d[a];
                 }
+                require(std::isfinite(ncells_d), "msk_hierarchy_create: non-finite cell grid");
                 // bound the cell count (points much sparser than delta): larger
                 // cells only add candidates, never lose neighbours
-                if (g.ncells <= 8 * n[l] + 4096) {
+                if (ncells_d <= 8.0 * (double)n[l] + 4096.0) {
+                    Grid g{};
+                    g.inv_cell = 1.0 / cell;
+                    g.ncells = 1;
+                    for (int a = 0; a < 3; ++a) {
+                        g.lo[a] = a < d ? h->lo[a] : 0.0;
+                        g.dim[a] = (int64_t)dims_d[a];
+                        g.ncells *= g.dim[a];
+                    }
                     D.g = g;
                     break;
                 }
@@ -225,6 +233,20 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
             double r2;
             memcpy(&r2, &mr[l], sizeof r2);
             require(r2 > 0.0, "msk_hierarchy_create: duplicate points in level " + std::to_string(l));
+            if (!q && !std::isfinite(r2) && n[l] > 1) {
+                // no pair within delta_l: widen the search (m cells per axis) until the
+                // closest pair found is closer than m cell sides -- then it is the closest
+                const LevelView v = h->view(l);
+                const double cell = 1.0 / v.g.inv_cell;
+                int64_t maxdim = 1;
+                for (int a = 0; a < d; ++a) maxdim = std::max<int64_t>(maxdim, v.g.dim[a]);
+                for (int64_t m = 2;; m *= 2) {
+                    const int mm = (int)std::min<int64_t>(m, maxdim);
+                    r2 = min_r2_reach(d, v, mm, st);
+                    const double lim = (double)mm * cell * (1.0 - 1e-12);
+                    if (mm >= maxdim || (std::isfinite(r2) && r2 < lim * lim)) break;
+                }
+            }
             h->lev[l].q = q ? q[l] : (std::isfinite(r2) ? 0.5 * sqrt(r2) : 0.5 * delta[l]);
         }
         h->t_create_ms = tm.ms();
@@ -449,18 +471,23 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     dfree(dstat, st); dfree(pstat, st); dfree(cptr, st); dfree(cpos, st); dfree(crow, st); dfree(ccol, st);
     h->lagrange_max_iters = std::max(hstat[1], hps[2]);
     h->patch_max_points = hps[3];
-    h->T = T;
-    h->T_active = T;
-    h->tmax_active = 255;
-    h->tnnz_active = h->tnnz;
     if (hstat[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: Lagrange CG did not converge in 20000 iterations");
     if (hps[1]) throw Error(MSK_ERR_INVALID, "msk_assemble: local patch overflow in " + std::to_string(hps[1]) +
                                                  " columns; reduce patch_R");
     if (hps[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: patch Lagrange CG did not converge in " +
                                                 std::to_string(hps[0]) + " columns");
+    // the factor is valid: only now does the hierarchy carry it
+    h->T = T;
+    h->T_active = T;
+    h->tmax_active = 255;
+    h->tnnz_active = h->tnnz;
 }
 
 }  // namespace
+
+namespace {
+void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch_R, int64_t patch_min_n, bool mf);
+}
 
 extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrange_tol, double patch_R,
                                       int64_t patch_min_n) {
@@ -474,9 +501,26 @@ extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrang
             "msk_assemble: the thresholded factor needs assembled A_l (hierarchy is MSK_FLAG_MATRIX_FREE)");
     const bool mf = (h->flags & MSK_FLAG_MATRIX_FREE) != 0;
     MSK_CUDA(cudaSetDevice(h->ctx->device));
-    cudaStream_t st = h->st();
+    // a failed (re-)assembly leaves the hierarchy unassembled (MSK_ERR_STATE for
+    // msk_solve), never with a half-built factor or freed CSR arrays
+    h->assembled = false;
+    h->solved = false;
     h->release_factor();
     h->release_dist();
+    try {
+        assemble_body(h, T, lagrange_tol, patch_R, patch_min_n, mf);
+    } catch (...) {
+        h->release_factor();
+        h->release_dist();
+        h->assembled = false;
+        throw;
+    }
+    API_END
+}
+
+namespace {
+void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch_R, int64_t patch_min_n, bool mf) {
+    cudaStream_t st = h->st();
     Timer tm(st);
     tm.start();
     int launches = 0;
@@ -611,8 +655,8 @@ extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrang
     h->t_assemble_ms = tm.ms();
     h->launches_assemble = launches;
     h->assembled = true;
-    API_END
 }
+}  // namespace
 
 extern "C" msk_status msk_assemble(msk_hierarchy *h, double T, double lagrange_tol) {
     return msk_assemble_ex(h, T, lagrange_tol, 0.0, 0);
@@ -768,6 +812,18 @@ extern "C" msk_status msk_export_cells(msk_hierarchy *h, int level, int32_t *per
         if (dims) dims[a] = D.g.dim[a];
     }
     if (cell) *cell = 1.0 / D.g.inv_cell;
+    API_END
+}
+
+extern "C" msk_status msk_export_grid(msk_hierarchy *h, int level, double *lo, double *inv_cell, int64_t *dims) {
+    API_BEGIN
+    require(h != nullptr && level >= 0 && level < h->L, "msk_export_grid: bad argument");
+    const LevelData &D = h->lev[level];
+    for (int a = 0; a < h->d; ++a) {
+        if (lo) lo[a] = D.g.lo[a];
+        if (dims) dims[a] = D.g.dim[a];
+    }
+    if (inv_cell) *inv_cell = D.g.inv_cell;
     API_END
 }
 

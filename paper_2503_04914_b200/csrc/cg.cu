@@ -41,6 +41,7 @@
 // all CTAs of a group take identical control flow.
 #include <cuda/atomic>
 
+#include <mutex>
 #include <vector>
 
 #include "kernels.cuh"
@@ -297,10 +298,18 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             if (ASYNC && kb + 2 * CAPTE < K1) {
                 // piece j + 2 lies in this chunk: the last warp to finish piece j
                 // refills its stage; the other warps go on without waiting
+                // Ordering: __syncwarp orders the warp's reads of the stage before
+                // lane 0's arrival; the arrival is a release (and the last one an
+                // acquire) at CTA scope, so every warp's generic-proxy reads of
+                // the stage happen-before the refill; fence.proxy.async then
+                // orders them before the async-proxy (TMA) write.
+                constexpr unsigned NW = NT / 32;
                 __syncwarp();
                 if ((tid & 31) == 0) {
-                    const unsigned old = atomicAdd(&S.arr[ps.P & 1], 1u);
-                    if ((old & 7u) == 7u) {
+                    cuda::atomic_ref<unsigned, cuda::thread_scope_block> arr(S.arr[ps.P & 1]);
+                    const unsigned old = arr.fetch_add(1u, cuda::memory_order_acq_rel);
+                    if (old % NW == NW - 1) {
+                        fence_proxy_async_smem();
                         const int64_t k2 = kb + 2 * CAPTE;
                         issue_piece_t(S, ps.P & 1, L.col, L.val, k2, k2 + CAPTE < K1 ? k2 + CAPTE : K1, pol);
                     }
@@ -1088,28 +1097,48 @@ struct CGVariant {
     size_t smem;
     int resident;  // co-resident CTAs of k_cg on the device
 };
-CGVariant g_var[3];
+// Per device: cudaFuncSetAttribute applies to the current device's context
+// only, and co-residency depends on the device.  Set once per device under a
+// mutex (several host threads -- e.g. the threaded-rank tests -- may race here).
+constexpr int kMaxDevices = 64;
+CGVariant g_var_dev[kMaxDevices][3];
+bool g_var_done[kMaxDevices] = {false};
+std::mutex g_var_mu;
+thread_local CGVariant *g_var = g_var_dev[0];
 
 void set_smem_attrs() {
-    static bool done = false;
-    if (done) return;
+    int dev = 0;
+    MSK_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) throw Error(3, "set_smem_attrs: device index out of range");
+    std::lock_guard<std::mutex> lk(g_var_mu);
+    g_var = g_var_dev[dev];
+    if (g_var_done[dev]) return;
     g_var[0] = {(const void *)k_cg<CAPT0, MINB0>, (const void *)k_dcg_spmv<CAPT0, MINB0>,
                 sizeof(CGSharedTT<CAPT0>), 0};
     g_var[1] = {(const void *)k_cg<CAPT1, MINB1>, (const void *)k_dcg_spmv<CAPT1, MINB1>,
                 sizeof(CGSharedTT<CAPT1>), 0};
     g_var[2] = {(const void *)k_cg<CAPT2, MINB2>, (const void *)k_dcg_spmv<CAPT2, MINB2>,
                 sizeof(CGSharedTT<CAPT2>), 0};
-    int dev = 0, sms = 0;
-    MSK_CUDA(cudaGetDevice(&dev));
+    int sms = 0;
     MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    for (auto &v : g_var) {
+    for (int vi = 0; vi < 3; ++vi) {
+        CGVariant &v = g_var[vi];
         MSK_CUDA(cudaFuncSetAttribute(v.cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
         MSK_CUDA(cudaFuncSetAttribute(v.dcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
         int per = 0;
         MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, v.cg, NT, v.smem));
         v.resident = sms * (per > 0 ? per : 1);
     }
-    done = true;
+    // the other dynamic-shared-memory kernels of this file (multi-RHS CG, plain SpMV)
+    MSK_CUDA(cudaFuncSetAttribute(k_cgr<2048, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(CGSharedR<2048, 2>)));
+    MSK_CUDA(cudaFuncSetAttribute(k_cgr<2048, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(CGSharedR<2048, 4>)));
+    MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT0, MINB0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(CGSharedTT<CAPT0>)));
+    MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT1, MINB1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(CGSharedTT<CAPT1>)));
+    g_var_done[dev] = true;
 }
 
 // variant by mean row length (entries per row of the work being launched)
@@ -1122,7 +1151,7 @@ int cg_variant(double nnz, double rows) { return rows > 0 && nnz >= MSK_LONGROW 
 int cg_max_resident_blocks() {
     set_smem_attrs();
     int r = g_var[0].resident;
-    for (const auto &v : g_var) r = v.resident < r ? v.resident : r;
+    for (int vi = 0; vi < 3; ++vi) r = g_var[vi].resident < r ? g_var[vi].resident : r;
     return r;
 }
 
@@ -1264,11 +1293,7 @@ void cg_multi(const CGRArgs &a, int R, cudaStream_t st, int *launches) {
     constexpr int CM = 2048;
     const void *fn = R == 2 ? (const void *)k_cgr<CM, 2, 2> : (const void *)k_cgr<CM, 2, 4>;
     const size_t smem = R == 2 ? sizeof(CGSharedR<CM, 2>) : sizeof(CGSharedR<CM, 4>);
-    static bool attr[2] = {false, false};
-    if (!attr[R == 4]) {
-        MSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[R == 4] = true;
-    }
+    set_smem_attrs();  // per device, includes k_cgr's attribute
     int dev = 0, sms = 0, per = 0;
     MSK_CUDA(cudaGetDevice(&dev));
     MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1352,15 +1377,7 @@ void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStr
 void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,
               const double *v, double *y, cudaStream_t st, int *launches) {
     if (n == 0) return;
-    set_smem_attrs();
-    static bool attr = false;
-    if (!attr) {
-        MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT0, MINB0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(CGSharedTT<CAPT0>)));
-        MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT1, MINB1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(CGSharedTT<CAPT1>)));
-        attr = true;
-    }
+    set_smem_attrs();  // per device, includes k_spmv_t's attribute
     CGLevelArgs L{};
     L.n = n;
     L.row_ptr = row_ptr;

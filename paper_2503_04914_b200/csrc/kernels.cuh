@@ -185,6 +185,7 @@ void dcg_xfin(const DistCGArgs &a, cudaStream_t st);
 void dcg_mf_spmv(const DistCGArgs &a, const LevelView &v, int d, int k, cudaStream_t st);
 // [lo, hi] of the column indices hit by rows (exact test): halo of a matrix-free partition
 void hit_range(int d, const LevelView &rows, const LevelView &cols, unsigned long long *mm, cudaStream_t st);
+double min_r2_reach(int d, const LevelView &v, int m, cudaStream_t st);
 void dcg_scalar(const DistCGArgs &a, int mode, cudaStream_t st);
 void sum_arrays(int W, const DistPtrs &srcs, double *dst, int64_t n, cudaStream_t st);
 void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStream_t st);

@@ -559,7 +559,14 @@ void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launc
     if (a.ncols <= 0) return;
     // a patch that does not fit in shared memory: a global workspace slice per
     // CTA of a persistent grid (slower, L2-resident vectors)
-    const bool global = smem > 227 * 1024;
+    // the opt-in limit minus the kernel's static shared memory (block reductions)
+    int dev = 0, optin = 0;
+    MSK_CUDA(cudaGetDevice(&dev));
+    MSK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    if (a.d == 2) MSK_CUDA(cudaFuncGetAttributes(&fa, a.k == 0 ? k_patch<2, 0> : a.k == 1 ? k_patch<2, 1> : k_patch<2, 2>));
+    else MSK_CUDA(cudaFuncGetAttributes(&fa, a.k == 0 ? k_patch<3, 0> : a.k == 1 ? k_patch<3, 1> : k_patch<3, 2>));
+    const bool global = smem + fa.sharedSizeBytes > (size_t)optin;
     unsigned grid = (unsigned)a.ncols;
     unsigned char *gws = nullptr;
     const size_t stride = (smem + 255) & ~(size_t)255;

@@ -67,6 +67,25 @@ HIERS = {
 
 
 # --------------------------------------------------------------- a1 cell list
+def _assert_keys_exact(P, c):
+    """Every sorted point's key equals the key map recomputed here from the
+    exported grid: floor((x - lo) * inv_cell) with one rounded subtraction and
+    one rounded multiplication (numpy evaluates each ufunc separately, so no
+    FMA: reading C-4), clamped to the grid, row-major x-major (reading C-26).
+    Bit-exact, no tolerance."""
+    Ps = P[c["perm"]]
+    dims = np.asarray(c["dims"], dtype=np.int64)
+    cc = np.floor((Ps - np.asarray(c["lo"])) * c["inv_cell"]).astype(np.int64)
+    cc = np.clip(cc, 0, dims - 1)
+    key = cc[:, 0]
+    for a in range(1, P.shape[1]):
+        key = key * dims[a] + cc[:, a]
+    assert np.array_equal(key, c["keys"])
+    # the key map is the grid the cell side describes
+    assert c["inv_cell"] == 1.0 / c["cell"] or abs(c["inv_cell"] * c["cell"] - 1.0) < 1e-15
+
+
+
 @pytest.mark.parametrize("name", ["C1", "halton3d", "grid5"])
 def test_cell_list_structure(msk, ctx, name):
     H = HIERS[name]()
@@ -80,11 +99,7 @@ def test_cell_list_structure(msk, ctx, name):
         same = keys[1:] == keys[:-1]
         assert np.all(perm[1:][same] > perm[:-1][same])                  # ties by caller index
         assert cs[0] == 0 and cs[-1] == H.n[l] and np.all(np.diff(cs) >= 0)
-        # each point lies in its cell (up to one rounding step of the key map)
-        idx = np.stack(np.unravel_index(keys, tuple(c["dims"])), axis=1)
-        lo = c["lo"] + idx * c["cell"]
-        Ps = P[perm]
-        assert np.all(Ps >= lo - 1e-12) and np.all(Ps <= lo + c["cell"] * (1 + 1e-12))
+        _assert_keys_exact(P, c)
         assert c["cell"] >= H.delta[l]
 
 
@@ -362,3 +377,40 @@ def test_c_example_runs(tmp_path):
     assert r.returncode == 0, r.stderr
     out = json.loads(r.stdout)
     assert out["points"] == [9, 25, 81] and out["max_interpolation_error"] < 1e-10
+
+
+def test_failed_reassemble_leaves_state_error(msk, ctx):
+    """A failed msk_assemble after a successful one leaves the hierarchy
+    unassembled: msk_solve must report MSK_ERR_STATE (never run on a half-built
+    factor or freed CSR arrays) until the next successful msk_assemble."""
+    H = HIERS["C1"]()
+    h = _hier(msk, ctx, H)
+    f = H.f()
+    a0, _ = h.solve(f, tol=TOL)
+    with pytest.raises(msk.MskError) as ei:   # Lagrange CG cannot reach 1e-300
+        h.assemble(T=3.0, lagrange_tol=1e-300)
+    assert ei.value.status == 5
+    with pytest.raises(msk.MskError) as ei:
+        h.solve(f, tol=TOL)
+    assert ei.value.status == 6
+    h.assemble()
+    a1, _ = h.solve(f, tol=TOL)
+    for l in range(H.L):
+        assert np.array_equal(a0[l], a1[l])
+
+
+@pytest.mark.parametrize("delta_scale", [1.0, 0.05])
+def test_q_null_is_exact_half_min_distance(msk, ctx, delta_scale):
+    """q = NULL: the library reports q_l = 1/2 min_{j != k} ||x_j - x_k||
+     exactly -- the oracle's brute-force separation (pinned by
+    Table 1 in test_oracle_pattern) -- also when delta_l is below the
+    separation (no pair within the support: widening cell search)."""
+    H = HIERS["C1"]()
+    delta = [dl * delta_scale for dl in H.delta]
+    h = msk.Hierarchy(ctx, H.points, delta, None, k=H.k)
+    info = h.info()
+    for l in range(H.L):
+        q = oracle.separation(H.points[l])
+        if delta_scale < 1:
+            assert 2 * q >= delta[l]          # the case the widening search exists for
+        assert abs(info.q[l] - q) <= 1e-15 * q, (l, info.q[l], q)

@@ -1,0 +1,125 @@
+"""Element-by-element parity at the sizes where the CG kernel changes shape.
+
+k_cg (cg.cu) picks its launch shape from the level size and the mean row
+length: 4-tile chunks (1024 rows) from 1024 tiles of 256 rows up, 2048-entry
+CSR pieces at 3 CTAs/SM for short rows (3-D) and 4096-entry pieces at 2
+CTAs/SM with the asynchronous stage release for long rows (2-D).  The
+hierarchies here reach those shapes and are still small enough for the plain
+CPU oracle (seconds to a minute):
+
+* C3P5 -- the 5-level prefix of C3 (d=3, finest level 1,250,000 points):
+  CH = 4 with the 2048-entry / 3-CTA pipeline;
+* C2P5 -- the 5-level prefix of C2 (d=2, finest level 262,144 points =
+  1024 tiles): CH = 4 with 4096-entry pieces (>= 3 per chunk), i.e. the
+  asynchronous stage release.
+
+Checked against the oracle (no sampling):
+* the sparsity pattern of A_l on the two finest levels and of the coupling
+  block B_{L,L-1}: bit-exact against oracle.pattern (its own bucket grid);
+* the cell keys of every level: bit-exact recompute (test_gpu_parity);
+* alpha per level: <= 1e-9 relative L2 against oracle.sequential at
+  tol 1e-12 (reading C-21; eq:mas P:284-290);
+* s_L at every one of the 1e5 evaluation points: against oracle.evaluate
+  from the GPU's own coefficients at the rounding bound of the kernel sum
+  (1e-14 x the sum with |alpha|; eq:fapproximation P:293-296), and against
+  oracle.evaluate from the oracle's coefficients within 1e-9 relative L2;
+* the matrix-free solve (MSK_FLAG_MATRIX_FREE) reproduces the assembled one
+  bit for bit at these shapes.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import config
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+BAR = 1e-9
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module", params=["C3P5", "C2P5"])
+def case(request):
+    import paper_2503_04914_b200 as msk
+    msk.load()
+    H = config(request.param)
+    f = H.f()
+    ctx = msk.Context(0)
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble()
+    a, info = h.solve(f, tol=TOL)
+    s, einfo = h.evaluate(H.eval_points)
+    cells = [h.export_cells(l) for l in range(H.L)]
+    blocks = {(rl, cl): h.export_block(rl, cl)[:2] for rl, cl in
+              [(H.L - 1, H.L - 1), (H.L - 2, H.L - 2), (H.L - 1, H.L - 2)]}
+    hm = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=msk.MSK_FLAG_MATRIX_FREE)
+    hm.assemble()
+    am, im = hm.solve(f, tol=TOL)
+    sm, _ = hm.evaluate(H.eval_points)
+    hm.close()
+    h.close()
+    ctx.close()
+    a_or, it_or, _ = oracle.sequential(H.points, H.delta, f, tol=TOL, k=H.k, direct_max_n=0)
+    return dict(H=H, f=f, a=a, info=info, s=s, einfo=einfo, cells=cells, blocks=blocks,
+                am=am, im=im, sm=sm, a_or=a_or, it_or=it_or)
+
+
+def test_launch_shape_reached(case):
+    """The finest level is large enough for 4-tile chunks (>= 1024 tiles)."""
+    H = case["H"]
+    assert H.n[-1] >= 1024 * 256
+    assert all(r <= TOL for r in case["info"].rel_res[:H.L])
+
+
+def test_cell_keys_exact(case):
+    from test_gpu_parity import _assert_keys_exact
+    H = case["H"]
+    for l in range(H.L):
+        _assert_keys_exact(H.points[l], case["cells"][l])
+
+
+def test_patterns_bitexact(case):
+    H = case["H"]
+    for (rl, cl), (rp, col) in case["blocks"].items():
+        orp, ocol = oracle.pattern(H.points[rl], H.points[cl], H.delta[cl], "grid")
+        assert np.array_equal(rp, orp), (rl, cl)
+        assert np.array_equal(col, ocol), (rl, cl)
+        if rl == cl:
+            assert case["info"] is not None
+
+
+def test_alpha_per_level(case):
+    H = case["H"]
+    for l in range(H.L):
+        e = _rel(case["a"][l], case["a_or"][l])
+        assert e < BAR, (H.name, l, e)
+        # same method, same stopping rule: iteration counts agree up to rounding
+        assert abs(case["info"].cg_iters[l] - case["it_or"][l]) <= max(2, case["it_or"][l] // 20)
+
+
+def test_evaluation_every_point(case):
+    H = case["H"]
+    x = H.eval_points
+    s = case["s"]
+    ref = oracle.evaluate(H.points, H.delta, case["a"], x, k=H.k)
+    scale = oracle.evaluate(H.points, H.delta, [np.abs(v) for v in case["a"]], x, k=H.k)
+    err = np.abs(s - ref)
+    assert np.all(err <= 1e-14 * scale + 1e-300), (err.max(), int(err.argmax()))
+    s_or = oracle.evaluate(H.points, H.delta, case["a_or"], x, k=H.k)
+    assert _rel(s, s_or) < BAR
+    # hit count of the evaluation kernel == the exact pattern size
+    nnz = sum(int(oracle.pattern(x, P, dl)[0][-1]) for P, dl in zip(H.points, H.delta))
+    assert case["einfo"].nnz == nnz
+
+
+def test_matrix_free_bitwise(case):
+    H = case["H"]
+    for l in range(H.L):
+        assert np.array_equal(case["am"][l], case["a"][l]), l
+        assert case["im"].cg_iters[l] == case["info"].cg_iters[l]
+    assert np.array_equal(case["sm"], case["s"])

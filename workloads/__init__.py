@@ -154,14 +154,17 @@ def config(name: str, m_eval=None) -> Hierarchy:
     C2: d=2, 6 levels N = 1024*4^(l-1) up to 1,048,576, nu=4.
     C3: d=3, 6 levels N = round(1e7 * 8^(l-6)) (305 ... 1e7), nu=1.5.
     C3P4/C3P5: the 4-/5-level prefixes of C3 (oracle-sized parity cases).
+    C2P5: the 5-level prefix of C2 (oracle-sized parity case).
     C5: d=2, 8 levels N = round(5e7 * 4^(l-8)), nu=4.
     """
     if name == "C1":
         return halton_hierarchy("C1", 2, [100, 400, 1600], 4.0,
                                 m_eval=10_000 if m_eval is None else m_eval)
-    if name == "C2":
-        return halton_hierarchy("C2", 2, [1024 * 4 ** l for l in range(6)], 4.0,
-                                m_eval=10_000 if m_eval is None else m_eval)
+    if name in ("C2", "C2P5"):
+        # C2P5: the 5-level prefix of C2 (finest level 262,144 points; oracle-sized)
+        L = 6 if name == "C2" else 5
+        return halton_hierarchy(name, 2, [1024 * 4 ** l for l in range(L)], 4.0,
+                                m_eval=(10_000 if name == "C2" else 100_000) if m_eval is None else m_eval)
     if name in ("C3", "C3P4", "C3P5", "C4", "C4F"):
         # C4 = the thresholded-factor study on the 4-level prefix of C3 (the
         # exact Lagrange build costs sum_l N(l)^2; SURVEY §8(d) C4); C4F = the
