@@ -20,12 +20,13 @@ p halos exchanged and CG chunk partials all-reduced over NCCL; smaller levels
 solved redundantly) -- strong scaling, DESIGN.md §Multi-GPU.  value = the
 problem's Wendland nonzeros per step (identical for every N: the partitioned
 solve reproduces the single-GPU iterations bit for bit) / max step time.
-`--impl reference` times the CPU oracle (oracle/, plain C, 1 thread) on a
-bounded sample of the same workload.
+`--impl reference` times the CPU oracle (oracle/, plain C; OpenMP over rows on
+the host's cores) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -233,11 +234,16 @@ def run_msk(args, rank, world, local_rank):
         cg_ms = float(np.mean([r[1].t_cg_ms for r in recs]))
         cg_bytes = float(np.mean([r[1].bytes_cg for r in recs]))
     achieved = cg_bytes / (cg_ms * 1e-3) / 1e9 if cg_ms > 0 else 0.0
+    # ncu DRAM bytes of this kernel, only if captured for THIS configuration
+    # (profiles/traffic_<round>.json, keyed by config and mode); else null
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp):
+    key = f"{args.config}{'_mf' if args.matrix_free else ''}_{sched}_T{thr:g}"
+    for tp in sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")), reverse=True):
         with open(tp) as fh:
-            traffic = json.load(fh).get("cg_finest_level_bytes_per_launch")
+            d = json.load(fh)
+        if key in d.get("cg_finest_level_bytes_per_launch_by_config", {}):
+            traffic = d["cg_finest_level_bytes_per_launch_by_config"][key]
+            break
     share = cg_ms / ms if ms > 0 else None
     if args.matrix_free:
         # FP64-ALU bound: algorithmic flops = 17 per Wendland nonzero (r^2 5, scale 1,
@@ -325,23 +331,67 @@ def oracle_step(H):
     return dt, nnz
 
 
-def cpu_baseline(args):
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+_SAMPLES = {
+    "C3P4": "4-level prefix of C3 (N=305..156250, 178,527 points)",
+    "C3P5": "5-level prefix of C3 (N=305..1.25e6, 1,428,527 points)",
+}
+
+
+def _oracle_leg(name, m_eval, threads):
+    """The oracle (same source as the tests' library) built -O3 -march=native
+    -ffp-contract=off -fopenmp for this host, `threads` OpenMP threads over rows
+    (reductions serial: bit-identical results for any thread count)."""
     import oracle
-    oracle.build()
-    name = "C3P4"
-    H = _oracle_sample(name, 100_000)
-    dt, nnz = oracle_step(H)
-    return {"value": nnz / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "seconds": dt,
-            "sample": f"{name}: 4-level prefix of C3 (N=305..156250, 178527 points), sequential eq:mas "
-                      f"solve (CG, tol 1e-12) + s_L at 1e5 uniform points; oracle/msk_oracle.c, gcc -O2, 1 thread"}
+    used = oracle.use_native(threads)
+    try:
+        dt, nnz = oracle_step(_oracle_sample(name, m_eval))
+    finally:
+        oracle.use_plain()
+    return {"value": nnz / dt / 1e9, "unit": UNIT, "cores": used, "seconds": dt,
+            "sample": f"{name}: {_SAMPLES[name]}, sequential eq:mas solve (CG, tol 1e-12) + s_L at "
+                      f"{m_eval:.0e} uniform points; oracle/msk_oracle.c gcc -O3 -march=native "
+                      f"-ffp-contract=off -fopenmp, {used} thread(s)"}
+
+
+def cpu_baseline(args):
+    """the oracle as it stands on this host, 1 thread (C3P4) and
+    OpenMP over rows on every core the job may use (C3P5); the reported value
+    is the multi-core leg."""
+    cores = _host_cores()
+    one = _oracle_leg("C3P4", 100_000, 1)
+    allc = _oracle_leg("C3P5", 1_000_000, cores)
+    out = dict(allc)
+    out.update({"kind": "oracle", "cpu_model": _cpu_model(), "host_cores": cores,
+                "legs": [one, allc]})
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the oracle on this host's cores (OpenMP build, all
+    affinity cores), each step one bounded sample (C3P4) of the workload."""
     import oracle
-    oracle.build()
+    cores = _host_cores()
     name = "C3P4"
     H = _oracle_sample(name, 100_000)
+    used = oracle.use_native(cores)
     for _ in range(args.warmup):
         oracle_step(H)
     ts, ns = [], []
@@ -349,15 +399,17 @@ def run_reference(args):
         dt, nnz = oracle_step(H)
         ts.append(dt)
         ns.append(nnz)
+    oracle.use_plain()
     ms = 1e3 * float(np.mean(ts))
     val = float(np.mean(ns)) / (ms * 1e-3) / 1e9
-    sample = (f"{name}: 4-level prefix of C3 (N=305..156250), sequential eq:mas solve (CG, tol 1e-12) "
-              f"+ s_L at 1e5 uniform points; oracle/msk_oracle.c, gcc -O2, 1 thread")
+    sample = (f"{name}: {_SAMPLES[name]}, sequential eq:mas solve (CG, tol 1e-12) + s_L at 1e5 uniform "
+              f"points; oracle/msk_oracle.c gcc -O3 -march=native -ffp-contract=off -fopenmp, {used} threads")
     return {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD, "sample": sample},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

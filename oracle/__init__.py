@@ -40,11 +40,48 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+NATIVE_FLAGS = ["-O3", "-march=native", "-ffp-contract=off", "-fno-fast-math", "-fopenmp"]
+
+
+def build_native() -> str:
+    """The same source for the CPU baseline: -O3 -march=native -ffp-contract=off
+    -fopenmp, compiled for THIS host into the temp directory (never shipped:
+    -march=native code may not run on another CPU).  Results are bit-identical
+    to build()'s library for any thread count (test_oracle_solvers.py)."""
+    import hashlib
+    import tempfile
+    with open(_SRC, "rb") as fh:
+        tag = hashlib.sha1(fh.read() + " ".join(NATIVE_FLAGS).encode()).hexdigest()[:12]
+    path = os.path.join(tempfile.gettempdir(), f"msk_oracle_native_{tag}_{os.getpid()}.so")
+    if not os.path.exists(path):
+        subprocess.check_call(["gcc"] + NATIVE_FLAGS + ["-fPIC", "-shared", "-o", path, _SRC, "-lm"])
+    return path
+
+
+def use_native(threads: int = 1) -> int:
+    """Switch this process's oracle calls to the native (-O3 -march=native
+    -fopenmp) build with `threads` OpenMP threads; returns the threads in
+    effect.  use_plain() switches back."""
+    global _lib
+    _lib = _load(build_native())
+    return int(_lib.mo_set_threads(int(threads)))
+
+
+def use_plain() -> None:
+    global _lib
+    _lib = None
+
+
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB)
+        _lib = _load(build())
+    return _lib
+
+
+def _load(path):
+    if True:
+        L = ctypes.CDLL(path)
         L.mo_phi.restype = ctypes.c_double
         L.mo_phi.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double]
         L.mo_kernel.restype = ctypes.c_double
@@ -87,8 +124,9 @@ def lib():
         L.mo_mas_row_residual.restype = ctypes.c_double
         L.mo_mas_row_residual.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, pp, _dp,
                                           pp, ctypes.c_double, ctypes.c_int64, _dp]
-        _lib = L
-    return _lib
+        L.mo_set_threads.restype = ctypes.c_int
+        L.mo_set_threads.argtypes = [ctypes.c_int]
+    return L
 
 
 # ---------------------------------------------------------------------------

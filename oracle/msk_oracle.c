@@ -14,6 +14,13 @@
  * -ffp-contract=off so that r^2 = ((dx*dx)+dy*dy)+dz*dz is evaluated left to
  * right without FMA (reading C-4).
  *
+ * Threads: built as it stands (no -fopenmp) every loop is serial.  The CPU
+ * baseline of bench.py also builds it with -fopenmp (-O3 -march=native): the
+ * pragmas below then split ROW loops (each row's result written by one
+ * thread, in the same order as serially) and elementwise vector updates over
+ * threads; every reduction (dot products, row sums) stays serial, so results
+ * are bit-identical for any thread count (tests/test_oracle_solvers.py).
+ *
  * Functions and their pins (tests/test_oracle_*.py):
  *   mo_phi, mo_kernel ........ closed forms phi(0)=1, phi(1/2)=0.1875,
  *                              phi(1)=0, Phi_2(r=1,d=2)=0.046875, C^{2k}
@@ -36,6 +43,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* ------------------------------------------------------------------------- */
 /* O1  Wendland functions and the scaled kernel                               */
@@ -204,6 +214,38 @@ int64_t mo_pattern_grid(int d, int64_t nr, const double *X, int64_t nc,
 {
     mo_grid g;
     if (grid_build(&g, d, nc, Y, delta)) return -1;
+#ifdef _OPENMP
+    /* threaded build: counts per row, a serial prefix, then the rows */
+    int fail = 0;
+#pragma omp parallel
+    {
+        int64_t *tb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc > 0 ? nc : 1));
+        if (!tb) {
+#pragma omp atomic write
+            fail = 1;
+        }
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t j = 0; j < nr; ++j)
+            row_ptr[j + 1] = tb ? grid_query(&g, X + j * d, delta, tb) : 0;
+#pragma omp single
+        {
+            row_ptr[0] = 0;
+            for (int64_t j = 0; j < nr; ++j) row_ptr[j + 1] += row_ptr[j];
+        }
+        if (col) {
+#pragma omp for schedule(dynamic, 1024)
+            for (int64_t j = 0; j < nr; ++j) {
+                if (!tb) continue;
+                int64_t cnt = grid_query(&g, X + j * d, delta, tb);
+                qsort(tb, (size_t)cnt, sizeof(int64_t), cmp_i64);
+                for (int64_t t = 0; t < cnt; ++t) col[row_ptr[j] + t] = (int32_t)tb[t];
+            }
+        }
+        free(tb);
+    }
+    grid_free(&g);
+    return fail ? -1 : row_ptr[nr];
+#endif
     int64_t *buf = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc > 0 ? nc : 1));
     if (!buf) { grid_free(&g); return -1; }
     int64_t nnz = 0;
@@ -228,6 +270,7 @@ void mo_values(int d, int k, double delta, int64_t nr, const double *X,
                const double *Y, const int64_t *row_ptr, const int32_t *col,
                double *val)
 {
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t j = 0; j < nr; ++j)
         for (int64_t p = row_ptr[j]; p < row_ptr[j + 1]; ++p)
             val[p] = mo_kernel(d, k, delta, X + j * d, Y + (int64_t)col[p] * d);
@@ -237,6 +280,7 @@ void mo_values(int d, int k, double delta, int64_t nr, const double *X,
 void mo_spmv(int64_t n, const int64_t *row_ptr, const int32_t *col,
              const double *val, const double *v, double *y)
 {
+#pragma omp parallel for schedule(static, 4096)
     for (int64_t j = 0; j < n; ++j) {
         double s = 0.0;
         for (int64_t p = row_ptr[j]; p < row_ptr[j + 1]; ++p) s += val[p] * v[col[p]];
@@ -250,19 +294,28 @@ int mo_apply(int d, int k, double delta, int64_t nr, const double *X,
 {
     mo_grid g;
     if (grid_build(&g, d, nc, Y, delta)) return -1;
-    int64_t *buf = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc > 0 ? nc : 1));
-    if (!buf) { grid_free(&g); return -1; }
-    for (int64_t j = 0; j < nr; ++j) {
-        int64_t cnt = grid_query(&g, X + j * d, delta, buf);
-        qsort(buf, (size_t)cnt, sizeof(int64_t), cmp_i64);
-        double s = 0.0;
-        for (int64_t t = 0; t < cnt; ++t)
-            s += mo_kernel(d, k, delta, X + j * d, Y + buf[t] * d) * v[buf[t]];
-        out[j] = s;
+    int fail = 0;
+#pragma omp parallel
+    {
+        int64_t *buf = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc > 0 ? nc : 1));
+        if (!buf) {
+#pragma omp atomic write
+            fail = 1;
+        }
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t j = 0; j < nr; ++j) {
+            if (!buf) continue;
+            int64_t cnt = grid_query(&g, X + j * d, delta, buf);
+            qsort(buf, (size_t)cnt, sizeof(int64_t), cmp_i64);
+            double s = 0.0;
+            for (int64_t t = 0; t < cnt; ++t)
+                s += mo_kernel(d, k, delta, X + j * d, Y + buf[t] * d) * v[buf[t]];
+            out[j] = s;
+        }
+        free(buf);
     }
-    free(buf);
     grid_free(&g);
-    return 0;
+    return fail ? -1 : 0;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -297,10 +350,13 @@ int mo_cg(int64_t n, const int64_t *row_ptr, const int32_t *col,
             if (it >= max_iter) { status = 1; break; }
             mo_spmv(n, row_ptr, col, val, p, q);
             double alpha = rr / dot(n, p, q);
+#pragma omp parallel for schedule(static, 4096)
             for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+#pragma omp parallel for schedule(static, 4096)
             for (int64_t i = 0; i < n; ++i) r[i] -= alpha * q[i];
             double rr_new = dot(n, r, r);
             double beta = rr_new / rr;
+#pragma omp parallel for schedule(static, 4096)
             for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
             rr = rr_new;
             ++it;
@@ -610,4 +666,17 @@ double mo_mas_row_residual(int d, int k, int l, const int64_t *n,
         }
     if (absrow) *absrow = a;
     return s - f_j;
+}
+
+/* Threads of the -fopenmp build (the CPU baseline's multi-core leg); returns
+ * the count in effect (1 when built without OpenMP). */
+int mo_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
 }

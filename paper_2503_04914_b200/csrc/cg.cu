@@ -47,6 +47,7 @@
 #include "kernels.cuh"
 #include "neighbors.cuh"
 #include "tma.cuh"
+#include "wscan.cuh"
 
 namespace msk {
 
@@ -1028,6 +1029,77 @@ __global__ void __launch_bounds__(NT, 4) k_mf_spmv(DistCGArgs A, LevelView V) {
     }
 }
 
+// k_mf_spmv with the warp-cooperative, shared-memory-staged candidate scan
+// (wscan.cuh): warp w of the CTA owns rows base + 32 w + lane of each tile --
+// the rows this thread owns in k_mf_spmv -- and the hits are the same, in the
+// same order, so w and the chunk partials are bit-identical.  Dynamic shared
+// memory: 8 x WarpSmem.
+template <int D, int K>
+__global__ void __launch_bounds__(NT, 2) k_mf_spmv_w(DistCGArgs A, LevelView V) {
+    if (!A.sc->active) return;
+    extern __shared__ __align__(16) unsigned char mf_smem[];
+    __shared__ double red[NT / 32 + 2];
+    wscan::WarpSmem &W = reinterpret_cast<wscan::WarpSmem *>(mf_smem)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const CGLevelArgs &L = A.L;
+    const int CH = L.chunk_tiles, tid = threadIdx.x;
+    const bool first = A.sc->it == 0;
+    const double alpha_prev = A.sc->alpha, beta = A.sc->beta;
+    const double *rv = L.r;
+    const double d2 = V.delta2, inv = V.inv_delta, scl = V.scale;
+    const double4 *__restrict__ rec = V.rec;
+    for (int64_t c = A.c0 + blockIdx.x; c < A.c1; c += gridDim.x) {
+        double dot = 0.0;
+        for (int t = 0; t < CH; ++t) {
+            const int64_t i = (c * CH + t) * NT + tid;
+            const bool on = i < L.n;
+            double x[3] = {0.0, 0.0, 0.0};
+            float xf[3] = {0.f, 0.f, 0.f};
+            if (on) {
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    x[a] = V.x[a][i];
+                    xf[a] = (float)(x[a] - V.g.lo[a]);
+                }
+            }
+            double acc = 0.0;
+            auto flush = [&](int nh) {
+                int h = 0;
+                for (; h + 1 < nh; h += 2) {  // two records in flight
+                    const int j0 = W.hl[h * 32 + lane], j1 = W.hl[(h + 1) * 32 + lane];
+                    const double4 R0 = rec[j0], R1 = rec[j1];
+                    const double p0 = rv[j0], p1 = rv[j1];
+                    const double y0[3] = {R0.x, R0.y, R0.z}, y1[3] = {R1.x, R1.y, R1.z};
+                    const double r20 = dist2_nofma<D>(x, y0), r21 = dist2_nofma<D>(x, y1);
+                    if (r20 < d2) acc = fma(scl * wendland<K>(sqrt(r20) * inv), p0, acc);
+                    if (r21 < d2) acc = fma(scl * wendland<K>(sqrt(r21) * inv), p1, acc);
+                }
+                if (h < nh) {
+                    const int j0 = W.hl[h * 32 + lane];
+                    const double4 R0 = rec[j0];
+                    const double y0[3] = {R0.x, R0.y, R0.z};
+                    const double r20 = dist2_nofma<D>(x, y0);
+                    if (r20 < d2) acc = fma(scl * wendland<K>(sqrt(r20) * inv), rv[j0], acc);
+                }
+            };
+            wscan::scan_level<D>(V, x, xf, on, W, flush);
+            if (on) {
+                // epilogue: the expressions of spmv_phase
+                const double ri = rv[i];
+                const double po = first ? 0.0 : L.p[i], qo = first ? 0.0 : L.q[i], xo = first ? 0.0 : L.x[i];
+                const double pn = first ? ri : ri + beta * po;
+                const double qn = first ? acc : acc + beta * qo;
+                L.p[i] = pn;
+                L.q[i] = qn;
+                L.x[i] = first ? 0.0 : xo + alpha_prev * po;
+                dot += pn * qn;
+            }
+        }
+        const double s = block_sum<NT>(dot, red);
+        if (tid == 0) A.part_send[c] = s;
+    }
+}
+
 // mode 0: after init (bb); 1: after SpMV (pq, alpha); 2: after the r update
 // (rr', beta); 3: end of iteration (it++, stopping test).  One CTA; the sum
 // over chunks uses the order of chunk_allreduce.
@@ -1128,6 +1200,15 @@ void set_smem_attrs() {
         int per = 0;
         MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, v.cg, NT, v.smem));
         v.resident = sms * (per > 0 ? per : 1);
+    }
+    {  // matrix-free SpMV with per-warp staged neighbourhoods
+        const int mfs = (int)(sizeof(wscan::WarpSmem) * (NT / 32));
+        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
+        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
+        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
+        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
+        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
+        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
     }
     // the other dynamic-shared-memory kernels of this file (multi-RHS CG, plain SpMV)
     MSK_CUDA(cudaFuncSetAttribute(k_cgr<2048, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1347,7 +1428,14 @@ void dcg_xfin(const DistCGArgs &a, cudaStream_t st) {
     MSK_CHECK_LAUNCH();
 }
 void dcg_mf_spmv(const DistCGArgs &a, const LevelView &v, int d, int k, cudaStream_t st) {
-#define MSK_MF(DD, KK) k_mf_spmv<DD, KK><<<dcg_grid(a, 4), NT, 0, st>>>(a, v)
+    set_smem_attrs();  // per device, includes k_mf_spmv_w's attribute
+    const bool v1 = gather_v1();
+    constexpr size_t mfs = sizeof(wscan::WarpSmem) * (NT / 32);
+#define MSK_MF(DD, KK)                                                                   \
+    do {                                                                                 \
+        if (v1) k_mf_spmv<DD, KK><<<dcg_grid(a, 4), NT, 0, st>>>(a, v);                  \
+        else k_mf_spmv_w<DD, KK><<<dcg_grid(a, 2), NT, mfs, st>>>(a, v);                 \
+    } while (0)
     if (d == 2) {
         if (k == 0) MSK_MF(2, 0); else if (k == 1) MSK_MF(2, 1); else MSK_MF(2, 2);
     } else {

@@ -20,8 +20,11 @@
 //   Evaluation (eq:fapproximation P:295): base = 0, sign = +1, all levels.
 #include <cmath>
 
+#include <stdlib.h>
+
 #include "kernels.cuh"
 #include "neighbors.cuh"
+#include "wscan.cuh"
 
 namespace msk {
 
@@ -130,6 +133,135 @@ __global__ void __launch_bounds__(NT, MSK_GMINB) k_gather(GatherArgs a) {
     }
     if (a.hits) {
         long long tot = block_sum_ll<NT>(hits, sm);
+        if (threadIdx.x == 0) atomicAdd(a.hits, (unsigned long long)tot);
+    }
+}
+
+// k_gather with the warp-cooperative, shared-memory-staged candidate scan
+// (wscan.cuh): same hits, same order, same arithmetic => bit-identical to
+// k_gather.  128-thread CTAs (4 warps x 10.5 KB of static shared memory).
+constexpr int NTW = 128;
+template <int D, int K>
+__global__ void __launch_bounds__(NTW, 4) k_gather_w(GatherArgs a) {
+    __shared__ wscan::WarpSmem Ws[NTW / 32];
+    __shared__ long long sm[NTW / 32 + 1];
+    wscan::WarpSmem &W = Ws[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * NTW + threadIdx.x;
+    const bool on = i < a.nt;
+    long long hits = 0;
+    double x[3] = {0.0, 0.0, 0.0};
+    float xf[3] = {0.f, 0.f, 0.f};
+    if (on) {
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            x[t] = a.tx[t][i];
+            xf[t] = (float)(x[t] - a.lev[0].g.lo[t]);  // same origin for every level
+        }
+    }
+    double acc = 0.0;
+    for (int l = 0; l < a.nlev; ++l) {
+        const LevelView &L = a.lev[l];
+        const double d2 = L.delta2, inv = L.inv_delta;
+        const double4 *__restrict__ rec = L.rec;
+        double s = 0.0;
+        auto flush = [&](int nh) {
+            int h = 0;
+            for (; h + 1 < nh; h += 2) {  // two records in flight
+                const double4 R0 = rec[W.hl[h * 32 + lane]], R1 = rec[W.hl[(h + 1) * 32 + lane]];
+                const double r20 = rec_dist2<D>(x, R0), r21 = rec_dist2<D>(x, R1);
+                if (r20 < d2) {
+                    s = fma(wendland<K>(sqrt(r20) * inv), rec_coef<D>(R0), s);
+                    ++hits;
+                }
+                if (r21 < d2) {
+                    s = fma(wendland<K>(sqrt(r21) * inv), rec_coef<D>(R1), s);
+                    ++hits;
+                }
+            }
+            if (h < nh) {
+                const double4 R0 = rec[W.hl[h * 32 + lane]];
+                const double r20 = rec_dist2<D>(x, R0);
+                if (r20 < d2) {
+                    s = fma(wendland<K>(sqrt(r20) * inv), rec_coef<D>(R0), s);
+                    ++hits;
+                }
+            }
+        };
+        wscan::scan_level<D>(L, x, xf, on, W, flush);
+        acc = fma(L.scale, s, acc);
+    }
+    if (on) {
+        double v = a.sign * acc;
+        if (a.base) v = a.base[a.base_perm ? a.base_perm[i] : i] + v;
+        a.out[a.out_perm ? a.out_perm[i] : i] = v;
+    }
+    if (a.hits) {
+        long long tot = block_sum_ll<NTW>(hits, sm);
+        if (threadIdx.x == 0) atomicAdd(a.hits, (unsigned long long)tot);
+    }
+}
+
+// k_gather_m with the warp-cooperative scan (bit-identical per column)
+template <int D, int K, int R>
+__global__ void __launch_bounds__(NTW, 3) k_gather_mw(GatherMArgs a) {
+    __shared__ wscan::WarpSmem Ws[NTW / 32];
+    __shared__ long long sm[NTW / 32 + 1];
+    wscan::WarpSmem &W = Ws[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * NTW + threadIdx.x;
+    const bool on = i < a.nt;
+    long long hits = 0;
+    double x[3] = {0.0, 0.0, 0.0};
+    float xf[3] = {0.f, 0.f, 0.f};
+    if (on) {
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            x[t] = a.tx[t][i];
+            xf[t] = (float)(x[t] - a.lev[0].g.lo[t]);
+        }
+    }
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int l = 0; l < a.nlev; ++l) {
+        const LevelView &L = a.lev[l];
+        const double d2 = L.delta2, inv = L.inv_delta;
+        const double4 *__restrict__ rec = L.rec;
+        const double *__restrict__ cf = a.coef[l];
+        const int64_t ldc = a.ldc;
+        double s[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[r] = 0.0;
+        auto flush = [&](int nh) {
+            for (int h = 0; h < nh; ++h) {
+                const int j = W.hl[h * 32 + lane];
+                const double4 Q = rec[j];
+                const double r2 = rec_dist2<D>(x, Q);
+                if (r2 < d2) {
+                    const double w = wendland<K>(sqrt(r2) * inv);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) s[r] = fma(w, cf[(int64_t)j * ldc + r], s[r]);
+                    ++hits;
+                }
+            }
+        };
+        wscan::scan_level<D>(L, x, xf, on, W, flush);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma(L.scale, s[r], acc[r]);
+    }
+    if (on) {
+        const int64_t bi = a.base_perm ? a.base_perm[i] : i;
+        const int64_t oi = a.out_perm ? a.out_perm[i] : i;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double v = a.sign * acc[r];
+            if (a.base) v = (r < a.bcols ? a.base[bi * a.ldb + a.bcol0 + r] : 0.0) + v;
+            if (r < a.wcols) a.out[oi * a.ldo + a.ocol0 + r] = v;
+        }
+    }
+    if (a.hits) {
+        long long tot = block_sum_ll<NTW>(hits, sm);
         if (threadIdx.x == 0) atomicAdd(a.hits, (unsigned long long)tot);
     }
 }
@@ -306,8 +438,28 @@ float prefilter_threshold(double delta, double M, int d) {
     return std::nextafter(f, INFINITY);
 }
 
+// MSK_GATHER_V1=1: the per-thread kernels (k_gather, k_gather_m) instead of
+// the warp-cooperative ones (same bits; A/B timing)
+bool gather_v1() {
+    static const bool v1 = getenv("MSK_GATHER_V1") != nullptr;
+    return v1;
+}
+
 void gather(const GatherArgs &a, cudaStream_t st, int *launches) {
     if (a.nt == 0) return;
+    if (!gather_v1()) {
+        const unsigned nbw = ceil_div_u(a.nt, NTW);
+#define MSK_GW(DD, KK) k_gather_w<DD, KK><<<nbw, NTW, 0, st>>>(a)
+        if (a.d == 2) {
+            if (a.k == 0) MSK_GW(2, 0); else if (a.k == 1) MSK_GW(2, 1); else MSK_GW(2, 2);
+        } else {
+            if (a.k == 0) MSK_GW(3, 0); else if (a.k == 1) MSK_GW(3, 1); else MSK_GW(3, 2);
+        }
+#undef MSK_GW
+        MSK_CHECK_LAUNCH();
+        if (launches) *launches += 1;
+        return;
+    }
     unsigned nb = ceil_div_u(a.nt, NT);
 #define MSK_G(DD, KK) k_gather<DD, KK><<<nb, NT, 0, st>>>(a)
     if (a.d == 2) {
@@ -324,7 +476,13 @@ void gather_multi(const GatherMArgs &a, cudaStream_t st, int *launches) {
     if (a.nt == 0) return;
     unsigned nb = ceil_div_u(a.nt, NT);
     if (a.R != 2 && a.R != 4) throw Error(1, "gather_multi: R must be 2 or 4");
-#define MSK_GM(DD, KK, RR) k_gather_m<DD, KK, RR><<<nb, NT, 0, st>>>(a)
+    const bool v1 = gather_v1();
+    const unsigned nbw = ceil_div_u(a.nt, NTW);
+#define MSK_GM(DD, KK, RR)                                               \
+    do {                                                                 \
+        if (v1) k_gather_m<DD, KK, RR><<<nb, NT, 0, st>>>(a);            \
+        else k_gather_mw<DD, KK, RR><<<nbw, NTW, 0, st>>>(a);            \
+    } while (0)
 #define MSK_GMK(DD, RR)                                                                  \
     do {                                                                               \
         if (a.k == 0) MSK_GM(DD, 0, RR); else if (a.k == 1) MSK_GM(DD, 1, RR); else MSK_GM(DD, 2, RR); \

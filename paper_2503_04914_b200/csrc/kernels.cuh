@@ -54,6 +54,8 @@ struct GatherArgs {
     unsigned long long *hits;
 };
 void gather(const GatherArgs &a, cudaStream_t st, int *launches);
+// MSK_GATHER_V1 set: the per-thread matrix-free kernels instead of the warp-cooperative ones
+bool gather_v1();
 // multi-RHS kernel sums (msk_solve_multi / msk_evaluate_multi): R coefficient
 // columns per source level (spatial rows, row stride ldc); per column the same
 // arithmetic, in the same order, as gather() -- bit-identical to R single runs.

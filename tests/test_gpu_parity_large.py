@@ -98,8 +98,13 @@ def test_alpha_per_level(case):
     for l in range(H.L):
         e = _rel(case["a"][l], case["a_or"][l])
         assert e < BAR, (H.name, l, e)
-        # same method, same stopping rule: iteration counts agree up to rounding
-        assert abs(case["info"].cg_iters[l] - case["it_or"][l]) <= max(2, case["it_or"][l] // 20)
+    # the finest level is solved at tol by both (the pruned schedule solves the
+    # coarser levels at the inner tol / 10, reading C-10, so they need more
+    # iterations than the oracle's tol): same stopping rule, same count up to rounding
+    it, it_or = case["info"].cg_iters[H.L - 1], case["it_or"][H.L - 1]
+    assert abs(it - it_or) <= max(2, it_or // 20), (it, it_or)
+    for l in range(H.L - 1):
+        assert case["info"].cg_iters[l] >= case["it_or"][l]
 
 
 def test_evaluation_every_point(case):

@@ -75,3 +75,31 @@ def test_cholesky_rejects_indefinite():
     val = np.array([1.0, 2.0, 2.0, 1.0])
     with pytest.raises(np.linalg.LinAlgError):
         oracle.cholesky_solve(rp, col, val, np.ones(2))
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_native_openmp_build_is_bitwise_identical(threads):
+    """The CPU baseline's build of the same oracle source (-O3 -march=native
+    -ffp-contract=off -fopenmp, rows split over threads, reductions serial) gives
+    the plain build's results bit for bit: patterns, sequential alpha (CG), and
+    the evaluation."""
+    from workloads import config
+    H = config("C3P4", m_eval=2000)
+    H.points, H.delta = H.points[:3], H.delta[:3]
+    f = H.f()
+    oracle.use_plain()
+    a0, it0, c0 = oracle.sequential(H.points, H.delta, f, tol=1e-12, direct_max_n=0)
+    s0 = oracle.evaluate(H.points, H.delta, a0, H.eval_points)
+    rp0, col0 = oracle.pattern(H.points[2], H.points[1], H.delta[1])
+    try:
+        assert oracle.use_native(threads) == threads
+        a1, it1, c1 = oracle.sequential(H.points, H.delta, f, tol=1e-12, direct_max_n=0)
+        s1 = oracle.evaluate(H.points, H.delta, a1, H.eval_points)
+        rp1, col1 = oracle.pattern(H.points[2], H.points[1], H.delta[1])
+    finally:
+        oracle.use_plain()
+    assert it0 == it1 and np.array_equal(c0, c1)
+    for l in range(3):
+        assert np.array_equal(a0[l], a1[l])
+    assert np.array_equal(s0, s1)
+    assert np.array_equal(rp0, rp1) and np.array_equal(col0, col1)
