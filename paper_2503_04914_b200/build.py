@@ -28,7 +28,12 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, bounds: bool = False) -> str:
+    """bounds=True: the device bounds-check build (-DMSK_BOUNDS, MSK_DASSERT in
+    common.cuh) into libmsk_bounds.so; load it with MSK_LIB_PATH."""
+    BUILD = os.path.join(HERE, "_build_bounds" if bounds else "_build")
+    LIB = os.path.join(HERE, "libmsk_bounds.so" if bounds else "libmsk.so")
+    extra = ["-DMSK_BOUNDS"] if bounds else []
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(HERE, "..", "include", "msk.h"))
@@ -37,7 +42,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o]
+            cmd = [NVCC] + ARCH + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o]
             jobs.append(cmd)
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,4 +61,4 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv, bounds="--bounds" in sys.argv))

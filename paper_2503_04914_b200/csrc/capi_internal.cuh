@@ -229,6 +229,12 @@ inline void require(bool ok, const std::string &msg) {
 
 using namespace capi;
 
+// warp-scan broadcast limit (wscan.cuh): MSK_WS_BR x 3^d cells (default 2.5)
+inline float ws_bcells(int d) {
+    static const double br = getenv("MSK_WS_BR") ? atof(getenv("MSK_WS_BR")) : 2.5;
+    return (float)(br * (d == 3 ? 27.0 : 9.0));
+}
+
 struct msk_hierarchy {
     msk_ctx *ctx = nullptr;
     int d = 0, L = 0, k = 0;
@@ -272,18 +278,39 @@ struct msk_hierarchy {
         double *val = nullptr;
         int64_t hlo = 0, hhi = 0;  // columns referenced by the owned rows: [hlo, hhi)
     };
+    // peer-memory buffers of a partitioned level for k_pcg on separate GPUs:
+    // this rank's r, chunk partials, result and barrier counters (cudaMalloc,
+    // exported by IPC handle), and every rank's as mapped in this process
+    struct PeerMem {
+        bool tried = false, ok = false;
+        double *r = nullptr, *part = nullptr, *alpha = nullptr;
+        unsigned long long *cnt = nullptr;  // xcnt, nbar, gbar
+        std::vector<double *> pr, ppart, palpha;
+        std::vector<unsigned long long *> pcnt;
+        std::vector<void *> opened;  // IPC-opened peer bases (closed on release)
+    };
     struct LevelDist {
         bool on = false;
         std::vector<int64_t> rows;       // world + 1 row bounds
         std::vector<int64_t> hlo, hhi;   // per rank
         std::vector<PartLocal> local;
+        PeerMem peer;
     };
     LevelDist dist[kMaxLevels];
 
     void release_dist() {
         cudaStream_t s = st();
+        bool any_peer = false;
+        for (int l = 0; l < kMaxLevels; ++l) any_peer = any_peer || dist[l].peer.tried;
+        if (any_peer) cudaStreamSynchronize(s);  // no kernel may still use peer memory
         for (int l = 0; l < kMaxLevels; ++l) {
             for (auto &P : dist[l].local) { dfree(P.rp, s); dfree(P.col, s); dfree(P.val, s); }
+            PeerMem &M = dist[l].peer;
+            for (void *p : M.opened) cudaIpcCloseMemHandle(p);
+            if (M.r) cudaFree(M.r);
+            if (M.part) cudaFree(M.part);
+            if (M.alpha) cudaFree(M.alpha);
+            if (M.cnt) cudaFree(M.cnt);
             dist[l] = LevelDist();
         }
     }
@@ -315,6 +342,7 @@ struct msk_hierarchy {
         v.rec = D.rec;
         v.frec = D.frec;
         v.fthr = D.fthr;
+        v.bcells = ws_bcells(d);
         return v;
     }
 

@@ -90,6 +90,79 @@ double cg_bytes(const LevelData &D, int iters) {
 
 }  // namespace capi
 
+namespace {
+// MSK_DIST_P2P=0: the partitioned CG as host-driven phase kernels with NCCL
+// collectives (or device copies in the emulation) instead of k_pcg
+bool dist_p2p_enabled() {
+    const char *e = getenv("MSK_DIST_P2P");
+    return !(e && e[0] == '0');
+}
+
+// Peer memory of partitioned level l for k_pcg across processes (one GPU per
+// rank): allocate this rank's r / partials / result / counters with cudaMalloc,
+// all-gather the IPC handles over NCCL, open the peers'.  Every rank makes the
+// same calls; a failure anywhere (e.g. ranks sharing one device in one process,
+// no peer access) is agreed on by an all-reduce and every rank falls back to
+// the phase path.  Done once per level and assembly (cached in dist[l].peer).
+bool peer_setup(msk_hierarchy *h, int l, int64_t nch) {
+    auto &M = h->dist[l].peer;
+    if (M.tried) return M.ok;
+    M.tried = true;
+    cudaStream_t st = h->st();
+    const int W = h->ctx->world, me = h->ctx->rank;
+    const int64_t n = h->lev[l].n;
+    int fail = 0;
+    auto ck = [&](cudaError_t e) {
+        if (e != cudaSuccess) { cudaGetLastError(); fail = 1; }
+    };
+    ck(cudaMalloc((void **)&M.r, sizeof(double) * (size_t)n));
+    ck(cudaMalloc((void **)&M.part, sizeof(double) * (size_t)(3 * nch)));
+    ck(cudaMalloc((void **)&M.alpha, sizeof(double) * (size_t)n));
+    ck(cudaMalloc((void **)&M.cnt, sizeof(unsigned long long) * 3));
+    constexpr int NB = 4;  // handles per rank
+    std::vector<cudaIpcMemHandle_t> mine(NB);
+    memset(mine.data(), 0, sizeof(cudaIpcMemHandle_t) * NB);
+    if (!fail) {
+        ck(cudaMemset(M.cnt, 0, sizeof(unsigned long long) * 3));
+        ck(cudaIpcGetMemHandle(&mine[0], M.r));
+        ck(cudaIpcGetMemHandle(&mine[1], M.part));
+        ck(cudaIpcGetMemHandle(&mine[2], M.alpha));
+        ck(cudaIpcGetMemHandle(&mine[3], M.cnt));
+    }
+    const size_t hb = sizeof(cudaIpcMemHandle_t) * NB;
+    unsigned char *dh = dalloc<unsigned char>(hb * (size_t)(W + 1), st);
+    MSK_CUDA(cudaMemcpyAsync(dh + hb * W, mine.data(), hb, cudaMemcpyHostToDevice, st));
+    MSK_NCCL(nccl_api()->AllGather(dh + hb * W, dh, hb, ncclUint8, h->ctx->comm, st));
+    std::vector<cudaIpcMemHandle_t> all((size_t)(NB * W));
+    MSK_CUDA(cudaMemcpyAsync(all.data(), dh, hb * W, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    M.pr.assign(W, nullptr); M.ppart.assign(W, nullptr); M.palpha.assign(W, nullptr); M.pcnt.assign(W, nullptr);
+    for (int w = 0; w < W && !fail; ++w) {
+        if (w == me) {
+            M.pr[w] = M.r; M.ppart[w] = M.part; M.palpha[w] = M.alpha; M.pcnt[w] = M.cnt;
+            continue;
+        }
+        void *p[NB] = {nullptr, nullptr, nullptr, nullptr};
+        for (int k = 0; k < NB && !fail; ++k) {
+            ck(cudaIpcOpenMemHandle(&p[k], all[(size_t)(NB * w + k)], cudaIpcMemLazyEnablePeerAccess));
+            if (!fail) M.opened.push_back(p[k]);
+        }
+        M.pr[w] = (double *)p[0]; M.ppart[w] = (double *)p[1]; M.palpha[w] = (double *)p[2];
+        M.pcnt[w] = (unsigned long long *)p[3];
+    }
+    // agreement: every rank takes the peer path, or none does
+    int *df = (int *)dh;
+    MSK_CUDA(cudaMemcpyAsync(df + 1, &fail, sizeof(int), cudaMemcpyHostToDevice, st));
+    MSK_NCCL(nccl_api()->AllReduce(df + 1, df, 1, ncclInt32, ncclSum, h->ctx->comm, st));
+    int tot = 0;
+    MSK_CUDA(cudaMemcpyAsync(&tot, df, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    dfree(dh, st);
+    M.ok = tot == 0;
+    return M.ok;
+}
+}  // namespace
+
 extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double tol,
                                 int32_t max_iter, uint32_t schedule, double *const *alpha,
                                 msk_solve_info *info) {
@@ -311,6 +384,103 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             }
         };
         if (mf) h->pack(l, h->ws_r(l), &launches);  // packed coordinates for k_mf_spmv
+        const bool p2p = part && !mf && dist_p2p_enabled() && (emu || peer_setup(h, l, nch));
+        if (p2p && !emu) {
+            // ---- one GPU per rank: this rank's k_pcg over the peers' mapped buffers
+            auto &M = Dd.peer;
+            const auto &P = Dd.local[0];
+            PeerCGArgs pa{};
+            pa.L = args[0].L;
+            pa.L.out_iters = d_it + l;
+            pa.L.out_rr = d_rr + 2 * l;
+            pa.L.out_status = d_stat + l;
+            pa.L.nnz = D.nnz;
+            pa.nchunks = nch;
+            pa.W = W;
+            pa.rank = h->ctx->rank;
+            pa.nb = pcg_resident_blocks((double)D.nnz, (double)n);
+            MSK_CUDA(cudaMemsetAsync(M.cnt + 2, 0, sizeof(unsigned long long), st));  // own group barrier
+            for (int w = 0; w < W; ++w) {
+                PeerRank &pr = pa.R[w];
+                pr.r = M.pr[w];
+                pr.part = M.ppart[w];
+                pr.alpha = M.palpha[w];
+                pr.xcnt = M.pcnt[w];
+                pr.nbar = M.pcnt[w] + 1;
+                pr.gbar = M.pcnt[w] + 2;
+                pr.hlo = Dd.hlo[w];
+                pr.hhi = Dd.hhi[w];
+                const int64_t cpr = (int64_t)CH * 256;
+                pr.c0 = Dd.rows[w] / cpr;
+                pr.c1 = (Dd.rows[w + 1] + cpr - 1) / cpr;
+                if (w == h->ctx->rank) {
+                    pr.x = X[0]; pr.p = Pv[0]; pr.q = Q[0];
+                    pr.row_ptr = P.rp - P.lo; pr.col = P.col; pr.val = P.val;
+                }
+            }
+            time_cg(l);
+            pcg_launch(pa, st);
+            launches += 1;
+            cg_t.back()->stop();
+            MSK_CUDA(cudaMemcpyAsync(alpha_sp[l], M.alpha, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+            permute_scatter(n, alpha_sp[l], D.perm, ad[l].ptr, st, &launches);
+            for (double *p : send) dfree(p, st);
+            dfree(recv, st);
+            dfree(sc, st);
+            return;
+        }
+        if (p2p && emu) {
+            // ---- the whole CG of the level in ONE launch over peer memory (k_pcg):
+            // every partition is a group of CTAs; partials and halo rows of r are
+            // stored into the other partitions' buffers, the groups meet in a
+            // device-side barrier
+            double *pbuf = dalloc<double>((size_t)(3 * nch * np), st);
+            unsigned long long *cnt = dalloc<unsigned long long>((size_t)(3 * np), st);
+            MSK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 3 * np, st));
+            PeerCGArgs pa{};
+            pa.L = args[0].L;
+            pa.L.x = pa.L.r = pa.L.p = pa.L.q = nullptr;
+            pa.L.out_iters = d_it + l;
+            pa.L.out_rr = d_rr + 2 * l;
+            pa.L.out_status = d_stat + l;
+            pa.L.nnz = D.nnz;
+            pa.nchunks = nch;
+            pa.W = np;
+            pa.rank = -1;
+            pa.nb = std::max(1, pcg_resident_blocks((double)D.nnz, (double)n) / np);
+            for (int i = 0; i < np; ++i) {
+                const auto &P = parts[i];
+                PeerRank &pr = pa.R[i];
+                pr.x = X[i];
+                pr.r = R[i];
+                pr.p = Pv[i];
+                pr.q = Q[i];
+                pr.part = pbuf + (size_t)(3 * nch) * i;
+                pr.alpha = alpha_sp[l];  // every partition pushes its owned rows into the one result
+                pr.xcnt = cnt + 3 * i;
+                pr.nbar = cnt + 3 * i + 1;
+                pr.gbar = cnt + 3 * i + 2;
+                pr.row_ptr = P.rp - P.lo;
+                pr.col = P.col;
+                pr.val = P.val;
+                pr.c0 = P.c0;
+                pr.c1 = P.c1;
+                pr.hlo = P.hlo;
+                pr.hhi = P.hhi;
+            }
+            time_cg(l);
+            pcg_launch(pa, st);
+            launches += 1;
+            cg_t.back()->stop();
+            dfree(pbuf, st);
+            dfree(cnt, st);
+            permute_scatter(n, alpha_sp[l], D.perm, ad[l].ptr, st, &launches);
+            for (double *p : owned_alloc) dfree(p, st);
+            for (double *p : send) dfree(p, st);
+            dfree(recv, st);
+            dfree(sc, st);
+            return;
+        }
         time_cg(l);
         for (int i = 0; i < np; ++i) dcg_init(args[i], st);
         allreduce();

@@ -182,10 +182,14 @@ __device__ __forceinline__ void issue_piece_t(SH &S, int b, const int32_t *col, 
 // 0, nloc = all chunks on one GPU; the owned chunk range of a partition in
 // the distributed CG).  L.row_ptr is indexed by global row.
 // PLAIN: y = A v only (msk_apply_block): v = L.r, y = L.q, no updates, no dot.
-template <int C, bool PLAIN = false>
+struct NoPush {
+    __device__ __forceinline__ void operator()(int64_t, double) const {}
+};
+template <int C, bool PLAIN = false, class Push = NoPush>
 __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
                                            int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol,
-                                           bool first, double alpha_prev, double beta) {
+                                           bool first, double alpha_prev, double beta,
+                                           const Push &push = Push()) {
     constexpr int CAPTE = C - 2;  // usable entries per piece (alignment slack)
     // Asynchronous stage release (pieces of >= MSK_ASYNC_MIN_C entries): when
     // piece j + 2 lies in the same chunk, the last warp to finish piece j
@@ -286,6 +290,8 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int ee = e + u;
+                        MSK_DASSERT(ee >= hi || (coff + ee < C + 8 && voff + ee < C && cur.col[coff + ee] >= 0 &&
+                                                 cur.col[coff + ee] < n));
                         pv[u] = ee < hi ? rv[cur.col[coff + ee]] : 0.0;
                         vv[u] = ee < hi ? cur.val[voff + ee] : 0.0;
                     }
@@ -359,7 +365,10 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
         }
         const double s = block_sum<NT>(dot, S.red);  // its barriers also retire rp buffer cs&1
         if (tid == 0) {
-            if (!PLAIN) part_out[cbase + me + k * nb] = s;
+            if (!PLAIN) {
+                part_out[cbase + me + k * nb] = s;
+                push(cbase + me + k * nb, s);  // partitioned CG over peer memory: the peers' copies
+            }
             if (k + 2 < K) {
                 int64_t nr0;
                 int nrows;
@@ -872,6 +881,177 @@ __device__ __forceinline__ void dcg_check_top(DistCGScalars &s, double tol2, int
     }
 }
 
+// ---------------------------------------------------------------------------
+// Partitioned CG over peer memory (PeerCGArgs, kernels.cuh).  One persistent
+// cooperative launch per rank runs the whole CG of its row block; W ranks in
+// ONE launch in the single-GPU emulation (rank = blockIdx.x / nb).
+__device__ __forceinline__ void red_release_sys_add(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// the fixed-order chunk sum of chunk_allreduce (no barrier: the caller's
+// cross-rank barrier has made every chunk partial visible)
+__device__ __forceinline__ double chunk_sum(const double *partials, int64_t nchunks, double *s_red) {
+    double t = 0.0;
+    for (int64_t j = threadIdx.x; j < nchunks; j += NT) t += __ldcg(&partials[j]);
+    return block_sum<NT>(t, s_red);
+}
+
+struct PeerPush {  // thread 0 stores a chunk partial into every rank's copy
+    const PeerCGArgs *A;
+    int64_t off;
+    __device__ __forceinline__ void operator()(int64_t c, double s) const {
+        for (int w = 0; w < A->W; ++w)
+            if (A->R[w].part) A->R[w].part[off + c] = s;
+    }
+};
+
+template <int C, int MB>
+__global__ void __launch_bounds__(NT, MB) k_pcg(const __grid_constant__ PeerCGArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CGSharedTT<C> &S = *reinterpret_cast<CGSharedTT<C> *>(smem_raw);
+    const int W = A.W, nb = A.nb, tid = threadIdx.x;
+    const int m = A.rank >= 0 ? A.rank : (int)blockIdx.x / nb;
+    const int me = (int)blockIdx.x - (A.rank >= 0 ? 0 : m * nb);
+    const PeerRank &Rm = A.R[m];
+    CGLevelArgs L = A.L;
+    L.x = Rm.x; L.r = Rm.r; L.p = Rm.p; L.q = Rm.q;
+    L.row_ptr = Rm.row_ptr; L.col = Rm.col; L.val = Rm.val;
+    const int64_t n = L.n, nch = A.nchunks, c0 = Rm.c0, c1 = Rm.c1;
+    const int CH = L.chunk_tiles;
+    double *part = Rm.part;
+    if (tid == 0) {
+        for (int b = 0; b < NSTG; ++b) mbar_init(&S.bar_st[b], 1);
+        mbar_init(&S.bar_rp[0], 1);
+        mbar_init(&S.bar_rp[1], 1);
+        S.arr[0] = S.arr[1] = 0u;
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    unsigned long long round = 0;
+    unsigned long long xround = *Rm.nbar;  // barriers of earlier launches (identical on every rank)
+    // cross-rank barrier: every thread's peer stores are fenced at system scope,
+    // the rank's CTAs meet (group barrier), its leader adds 1 to every rank's
+    // counter (release, system scope), every CTA waits for W arrivals (acquire)
+    auto xbarrier = [&]() {
+        __threadfence_system();
+        group_barrier(Rm.gbar, nb, round);
+        ++xround;
+        if (me == 0 && tid == 0)
+            for (int w = 0; w < W; ++w) red_release_sys_add(A.R[w].xcnt, 1ull);
+        if (tid == 0) {
+            const unsigned long long want = (unsigned long long)W * xround;
+            unsigned long long spins = 0;
+            while (ld_acquire_sys(Rm.xcnt) < want) {
+                __nanosleep(64);
+                if (++spins > (1ull << 31)) __trap();  // never hang the device forever
+            }
+        }
+        __syncthreads();
+    };
+    // r of a row this rank owns -> the peers whose SpMV reads it (their halo)
+    auto push_halo = [&](int64_t i, double v) {
+        for (int w = 0; w < W; ++w)
+            if (w != m && i >= A.R[w].hlo && i < A.R[w].hhi) A.R[w].r[i] = v;
+    };
+    auto push_part = [&](int64_t off, int64_t c, double v) {
+        for (int w = 0; w < W; ++w) A.R[w].part[off + c] = v;
+    };
+
+    // ---- init: r = b on the owned rows (+ halo copies), bb partials
+    for (int64_t c = c0 + me; c < c1; c += nb) {
+        double acc = 0.0;
+        for (int t = 0; t < CH; ++t) {
+            const int64_t i = (c * CH + t) * NT + tid;
+            if (i < n) {
+                const double bi = L.b_src ? __ldg(&L.b_src[__ldg(&L.b_perm[i])]) : __ldg(&L.b[i]);
+                L.r[i] = bi;
+                push_halo(i, bi);
+                acc += bi * bi;
+            }
+        }
+        const double s = block_sum<NT>(acc, S.red);
+        if (tid == 0) push_part(0, c, s);
+    }
+    xbarrier();
+    const double bb = chunk_sum(part, nch, S.red);
+    double rr = bb;
+    int it = 0, status = 0;
+    double alpha = 0.0, beta = 0.0;
+    PipeState ps{0u, 0u};
+    const PeerPush pq_push{&A, nch};
+    if (bb > 0.0) {
+        const double stop = L.tol2 * bb;
+        for (;;) {
+            if (rr <= stop) break;
+            if (it >= L.max_iter) { status = 1; break; }
+            // ---- w = A r ; p = r + beta p ; q = w + beta q ; x += alpha p_old ; pq partials
+            spmv_phase<C, false, PeerPush>(S, L, me, nb, c0, c1 - c0, CH, part + nch, ps, pol, it == 0, alpha,
+                                           beta, pq_push);
+            xbarrier();
+            const double pq = chunk_sum(part + nch, nch, S.red);
+            alpha = rr / pq;
+            if (L.coef && m == 0 && me == 0 && tid == 0 && it < L.coef_cap) L.coef[2 * it] = alpha;
+            // ---- r -= alpha q on the owned rows (+ halo copies), rr' partials
+            for (int64_t c = c0 + me; c < c1; c += nb) {
+                double rv[MAXCH], qv[MAXCH];
+#pragma unroll
+                for (int t = 0; t < MAXCH; ++t) {
+                    const int64_t i = (c * CH + t) * NT + tid;
+                    const bool ok = t < CH && i < n;
+                    rv[t] = ok ? L.r[i] : 0.0;
+                    qv[t] = ok ? L.q[i] : 0.0;
+                }
+                double acc = 0.0;
+#pragma unroll
+                for (int t = 0; t < MAXCH; ++t) {
+                    const int64_t i = (c * CH + t) * NT + tid;
+                    if (t < CH && i < n) {
+                        const double ri = rv[t] - alpha * qv[t];
+                        L.r[i] = ri;
+                        push_halo(i, ri);
+                        acc += ri * ri;
+                    }
+                }
+                const double s = block_sum<NT>(acc, S.red);
+                if (tid == 0) push_part(2 * nch, c, s);
+            }
+            xbarrier();
+            const double rrn = chunk_sum(part + 2 * nch, nch, S.red);
+            beta = rrn / rr;
+            rr = rrn;
+            if (L.coef && m == 0 && me == 0 && tid == 0 && it < L.coef_cap) L.coef[2 * it + 1] = beta;
+            ++it;
+        }
+    }
+    // ---- the last deferred x += alpha p on the owned rows, pushed to every rank's alpha
+    for (int64_t c = c0 + me; c < c1; c += nb)
+        for (int t = 0; t < CH; ++t) {
+            const int64_t i = (c * CH + t) * NT + tid;
+            if (i < n) {
+                const double xi = it > 0 ? L.x[i] + alpha * L.p[i] : 0.0;
+                L.x[i] = xi;
+                for (int w = 0; w < W; ++w) A.R[w].alpha[i] = xi;
+            }
+        }
+    xbarrier();
+    if (me == 0 && tid == 0) {
+        *Rm.nbar = xround;
+        if (m == 0 || A.rank >= 0) {
+            *L.out_iters = it;
+            L.out_rr[0] = rr;
+            L.out_rr[1] = bb;
+            *L.out_status = status;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NT) k_dcg_init(DistCGArgs A) {
     __shared__ double red[NT / 32 + 2];
     const CGLevelArgs &L = A.L;
@@ -1033,14 +1213,13 @@ __global__ void __launch_bounds__(NT, 4) k_mf_spmv(DistCGArgs A, LevelView V) {
 // (wscan.cuh): warp w of the CTA owns rows base + 32 w + lane of each tile --
 // the rows this thread owns in k_mf_spmv -- and the hits are the same, in the
 // same order, so w and the chunk partials are bit-identical.  Dynamic shared
-// memory: 8 x WarpSmem.
+// memory: 8 x WarpSmem (static).
 template <int D, int K>
-__global__ void __launch_bounds__(NT, 2) k_mf_spmv_w(DistCGArgs A, LevelView V) {
+__global__ void __launch_bounds__(NT, 3) k_mf_spmv_w(DistCGArgs A, LevelView V) {
     if (!A.sc->active) return;
-    extern __shared__ __align__(16) unsigned char mf_smem[];
+    __shared__ wscan::WarpSmem Ws[NT / 32];
     __shared__ double red[NT / 32 + 2];
-    wscan::WarpSmem &W = reinterpret_cast<wscan::WarpSmem *>(mf_smem)[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
+    wscan::WarpSmem &W = Ws[threadIdx.x >> 5];
     const CGLevelArgs &L = A.L;
     const int CH = L.chunk_tiles, tid = threadIdx.x;
     const bool first = A.sc->it == 0;
@@ -1063,10 +1242,11 @@ __global__ void __launch_bounds__(NT, 2) k_mf_spmv_w(DistCGArgs A, LevelView V) 
                 }
             }
             double acc = 0.0;
+            int hl[wscan::HM];
             auto flush = [&](int nh) {
                 int h = 0;
                 for (; h + 1 < nh; h += 2) {  // two records in flight
-                    const int j0 = W.hl[h * 32 + lane], j1 = W.hl[(h + 1) * 32 + lane];
+                    const int j0 = hl[h], j1 = hl[h + 1];
                     const double4 R0 = rec[j0], R1 = rec[j1];
                     const double p0 = rv[j0], p1 = rv[j1];
                     const double y0[3] = {R0.x, R0.y, R0.z}, y1[3] = {R1.x, R1.y, R1.z};
@@ -1075,14 +1255,14 @@ __global__ void __launch_bounds__(NT, 2) k_mf_spmv_w(DistCGArgs A, LevelView V) 
                     if (r21 < d2) acc = fma(scl * wendland<K>(sqrt(r21) * inv), p1, acc);
                 }
                 if (h < nh) {
-                    const int j0 = W.hl[h * 32 + lane];
+                    const int j0 = hl[h];
                     const double4 R0 = rec[j0];
                     const double y0[3] = {R0.x, R0.y, R0.z};
                     const double r20 = dist2_nofma<D>(x, y0);
                     if (r20 < d2) acc = fma(scl * wendland<K>(sqrt(r20) * inv), rv[j0], acc);
                 }
             };
-            wscan::scan_level<D>(V, x, xf, on, W, flush);
+            wscan::scan_level<D>(V, x, xf, on, W, hl, flush);
             if (on) {
                 // epilogue: the expressions of spmv_phase
                 const double ri = rv[i];
@@ -1201,15 +1381,10 @@ void set_smem_attrs() {
         MSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, v.cg, NT, v.smem));
         v.resident = sms * (per > 0 ? per : 1);
     }
-    {  // matrix-free SpMV with per-warp staged neighbourhoods
-        const int mfs = (int)(sizeof(wscan::WarpSmem) * (NT / 32));
-        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
-        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
-        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
-        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
-        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
-        MSK_CUDA(cudaFuncSetAttribute(k_mf_spmv_w<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mfs));
-    }
+    MSK_CUDA(cudaFuncSetAttribute(k_pcg<CAPT0, MINB0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(CGSharedTT<CAPT0>)));
+    MSK_CUDA(cudaFuncSetAttribute(k_pcg<CAPT1, MINB1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(CGSharedTT<CAPT1>)));
     // the other dynamic-shared-memory kernels of this file (multi-RHS CG, plain SpMV)
     MSK_CUDA(cudaFuncSetAttribute(k_cgr<2048, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(CGSharedR<2048, 2>)));
@@ -1408,6 +1583,25 @@ unsigned dcg_grid(const DistCGArgs &a, int per_sm) {
 }
 }  // namespace
 
+// co-resident CTAs of k_pcg's variant for a level (the per-rank grid is
+// this / W in the emulation, all of it on a GPU of its own)
+int pcg_resident_blocks(double nnz, double rows) {
+    set_smem_attrs();
+    return g_var[cg_variant(nnz, rows)].resident;
+}
+
+void pcg_launch(const PeerCGArgs &a, cudaStream_t st) {
+    set_smem_attrs();
+    const int vi = cg_variant((double)a.L.nnz, (double)a.L.n);
+    const CGVariant &var = g_var[vi];
+    const void *fn = vi == 0 ? (const void *)k_pcg<CAPT0, MINB0> : (const void *)k_pcg<CAPT1, MINB1>;
+    const unsigned grid = (unsigned)(a.rank >= 0 ? a.nb : a.nb * a.W);
+    if ((int)grid > var.resident) throw Error(3, "pcg_launch: grid exceeds the co-resident CTAs");
+    PeerCGArgs A = a;
+    void *args[] = {&A};
+    MSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NT), args, var.smem, st));
+}
+
 void dcg_init(const DistCGArgs &a, cudaStream_t st) {
     k_dcg_init<<<dcg_grid(a, 8), NT, 0, st>>>(a);
     MSK_CHECK_LAUNCH();
@@ -1428,13 +1622,11 @@ void dcg_xfin(const DistCGArgs &a, cudaStream_t st) {
     MSK_CHECK_LAUNCH();
 }
 void dcg_mf_spmv(const DistCGArgs &a, const LevelView &v, int d, int k, cudaStream_t st) {
-    set_smem_attrs();  // per device, includes k_mf_spmv_w's attribute
     const bool v1 = gather_v1();
-    constexpr size_t mfs = sizeof(wscan::WarpSmem) * (NT / 32);
 #define MSK_MF(DD, KK)                                                                   \
     do {                                                                                 \
         if (v1) k_mf_spmv<DD, KK><<<dcg_grid(a, 4), NT, 0, st>>>(a, v);                  \
-        else k_mf_spmv_w<DD, KK><<<dcg_grid(a, 2), NT, mfs, st>>>(a, v);                 \
+        else k_mf_spmv_w<DD, KK><<<dcg_grid(a, 3), NT, 0, st>>>(a, v);                   \
     } while (0)
     if (d == 2) {
         if (k == 0) MSK_MF(2, 0); else if (k == 1) MSK_MF(2, 1); else MSK_MF(2, 2);

@@ -29,6 +29,26 @@ struct Error : std::runtime_error {
 
 #define MSK_CHECK_LAUNCH() MSK_CUDA(cudaGetLastError())
 
+// Device-side bounds checks of the bounds build (python -m
+// paper_2503_04914_b200.build --bounds -> libmsk_bounds.so; the stand-in for
+// compute-sanitizer memcheck, which this GPU pool does not offer): a failed
+// check prints its location and traps (the launch fails with an error).
+#ifdef MSK_BOUNDS
+#include <cstdio>
+#define MSK_DASSERT(c)                                                                      \
+    do {                                                                                     \
+        if (!(c)) {                                                                          \
+            printf("MSK_DASSERT failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,   \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                                   \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define MSK_DASSERT(c) \
+    do {               \
+    } while (0)
+#endif
+
 // MSK_DEBUG_SYNC=1: synchronise after each orchestrated launch and name the
 // failing step (diagnostics for device faults; off by default).
 inline void debug_sync(cudaStream_t st, const char *what) {
@@ -66,6 +86,7 @@ struct LevelView {
     const double4 *rec;         // packed (x, y, z, coef) records (2-D: (x, y, coef, 0)) for gathers
     const float4 *frec;         // FP32 coordinates relative to g.lo (conservative prefilter)
     float fthr;                 // prefilter threshold: r2_f >= fthr  =>  r^2 >= delta^2 for sure
+    float bcells;               // warp scans (wscan.cuh): broadcast when the warp's box has <= bcells cells
 };
 
 // squared distance, left to right, round-to-nearest, no FMA (reading C-4)

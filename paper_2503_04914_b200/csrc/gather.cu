@@ -137,16 +137,18 @@ __global__ void __launch_bounds__(NT, MSK_GMINB) k_gather(GatherArgs a) {
     }
 }
 
-// k_gather with the warp-cooperative, shared-memory-staged candidate scan
-// (wscan.cuh): same hits, same order, same arithmetic => bit-identical to
-// k_gather.  128-thread CTAs (4 warps x 10.5 KB of static shared memory).
+// k_gather with the warp-cooperative candidate scan (wscan.cuh): same hits,
+// same order, same arithmetic => bit-identical to k_gather.  128-thread CTAs
+// (4 warps x 4.8 KB of static shared memory).
 constexpr int NTW = 128;
+#ifndef MSK_GW_MINB
+#define MSK_GW_MINB 6
+#endif
 template <int D, int K>
-__global__ void __launch_bounds__(NTW, 4) k_gather_w(GatherArgs a) {
+__global__ void __launch_bounds__(NTW, MSK_GW_MINB) k_gather_w(GatherArgs a) {
     __shared__ wscan::WarpSmem Ws[NTW / 32];
     __shared__ long long sm[NTW / 32 + 1];
     wscan::WarpSmem &W = Ws[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * NTW + threadIdx.x;
     const bool on = i < a.nt;
     long long hits = 0;
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(NTW, 4) k_gather_w(GatherArgs a) {
         }
     }
     double acc = 0.0;
+    int hl[wscan::HM];
     for (int l = 0; l < a.nlev; ++l) {
         const LevelView &L = a.lev[l];
         const double d2 = L.delta2, inv = L.inv_delta;
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(NTW, 4) k_gather_w(GatherArgs a) {
         auto flush = [&](int nh) {
             int h = 0;
             for (; h + 1 < nh; h += 2) {  // two records in flight
-                const double4 R0 = rec[W.hl[h * 32 + lane]], R1 = rec[W.hl[(h + 1) * 32 + lane]];
+                const double4 R0 = rec[hl[h]], R1 = rec[hl[h + 1]];
                 const double r20 = rec_dist2<D>(x, R0), r21 = rec_dist2<D>(x, R1);
                 if (r20 < d2) {
                     s = fma(wendland<K>(sqrt(r20) * inv), rec_coef<D>(R0), s);
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(NTW, 4) k_gather_w(GatherArgs a) {
                 }
             }
             if (h < nh) {
-                const double4 R0 = rec[W.hl[h * 32 + lane]];
+                const double4 R0 = rec[hl[h]];
                 const double r20 = rec_dist2<D>(x, R0);
                 if (r20 < d2) {
                     s = fma(wendland<K>(sqrt(r20) * inv), rec_coef<D>(R0), s);
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(NTW, 4) k_gather_w(GatherArgs a) {
                 }
             }
         };
-        wscan::scan_level<D>(L, x, xf, on, W, flush);
+        wscan::scan_level<D>(L, x, xf, on, W, hl, flush);
         acc = fma(L.scale, s, acc);
     }
     if (on) {
@@ -208,7 +211,6 @@ __global__ void __launch_bounds__(NTW, 3) k_gather_mw(GatherMArgs a) {
     __shared__ wscan::WarpSmem Ws[NTW / 32];
     __shared__ long long sm[NTW / 32 + 1];
     wscan::WarpSmem &W = Ws[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * NTW + threadIdx.x;
     const bool on = i < a.nt;
     long long hits = 0;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(NTW, 3) k_gather_mw(GatherMArgs a) {
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int hl[wscan::HM];
     for (int l = 0; l < a.nlev; ++l) {
         const LevelView &L = a.lev[l];
         const double d2 = L.delta2, inv = L.inv_delta;
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(NTW, 3) k_gather_mw(GatherMArgs a) {
         for (int r = 0; r < R; ++r) s[r] = 0.0;
         auto flush = [&](int nh) {
             for (int h = 0; h < nh; ++h) {
-                const int j = W.hl[h * 32 + lane];
+                const int j = hl[h];
                 const double4 Q = rec[j];
                 const double r2 = rec_dist2<D>(x, Q);
                 if (r2 < d2) {
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(NTW, 3) k_gather_mw(GatherMArgs a) {
                 }
             }
         };
-        wscan::scan_level<D>(L, x, xf, on, W, flush);
+        wscan::scan_level<D>(L, x, xf, on, W, hl, flush);
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = fma(L.scale, s[r], acc[r]);
     }
@@ -438,10 +441,13 @@ float prefilter_threshold(double delta, double M, int d) {
     return std::nextafter(f, INFINITY);
 }
 
-// MSK_GATHER_V1=1: the per-thread kernels (k_gather, k_gather_m) instead of
-// the warp-cooperative ones (same bits; A/B timing)
+// The per-thread kernels (k_gather, k_gather_m, k_mf_spmv) are the default;
+// MSK_GATHER_WARP=1 selects the warp-cooperative ones (wscan.cuh; same bits).
+// Same-box A/B on C3: B products 5.23 ms per-thread vs 6.2-7.6
+// warp (broadcast threshold 0 .. 4 x 3^d cells), evaluation 5.95 vs 7.0-8.2 --
+// the broadcast scan costs more instructions than the loads it saves.
 bool gather_v1() {
-    static const bool v1 = getenv("MSK_GATHER_V1") != nullptr;
+    static const bool v1 = getenv("MSK_GATHER_WARP") == nullptr || getenv("MSK_GATHER_V1") != nullptr;
     return v1;
 }
 

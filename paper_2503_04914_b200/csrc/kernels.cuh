@@ -54,7 +54,8 @@ struct GatherArgs {
     unsigned long long *hits;
 };
 void gather(const GatherArgs &a, cudaStream_t st, int *launches);
-// MSK_GATHER_V1 set: the per-thread matrix-free kernels instead of the warp-cooperative ones
+// true unless MSK_GATHER_WARP is set: the per-thread matrix-free kernels (default)
+// instead of the warp-cooperative ones (wscan.cuh)
 bool gather_v1();
 // multi-RHS kernel sums (msk_solve_multi / msk_evaluate_multi): R coefficient
 // columns per source level (spatial rows, row stride ldc); per column the same
@@ -196,6 +197,40 @@ void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStr
 // CSR arrays must be 16-byte aligned and padded: row_ptr n+3 entries,
 // col nnz+4, val nnz+2 (bulk copies round their extents to 16 bytes).
 int cg_max_resident_blocks();
+
+// ---- partitioned CG over peer memory (cg.cu k_pcg): the
+// whole CG of a row-partitioned level in ONE persistent launch per rank.
+// Chunk partials and halo rows of r are STORED into the peers' buffers (NVLink
+// peer pointers, IPC-mapped; or, in the single-GPU emulation, the other
+// partitions' buffers), and the ranks meet in a device-side barrier on
+// counters in each rank's memory (release/acquire at system scope) -- no host
+// round trip, no NCCL call, no launch per phase.  Same chunk partials and the
+// same fixed-order sums as k_cg => bit-identical to the single-GPU solve.
+struct PeerRank {
+    double *x, *r, *p, *q;      // this rank's vectors (global row index space; owned rows, r also its halo)
+    double *part;               // 3 * nchunks chunk partials (every rank pushes its chunks into every copy)
+    double *alpha;              // full-length result (every rank pushes its owned x)
+    unsigned long long *xcnt;   // cross-rank arrival counter (every rank adds 1 per barrier; never reset)
+    unsigned long long *nbar;   // barriers completed by earlier launches (this rank's copy)
+    unsigned long long *gbar;   // this rank's group-barrier counter (own CTAs; zeroed before the launch)
+    const int64_t *row_ptr;     // owned rows' CSR, indexed by global row
+    const int32_t *col;
+    const double *val;
+    int64_t c0, c1;             // owned chunks [c0, c1)
+    int64_t hlo, hhi;           // rows this rank's SpMV reads (owned rows and halo)
+};
+struct PeerCGArgs {
+    CGLevelArgs L;              // n, nnz, b / b_src / b_perm, tol2, max_iter, chunk_tiles, out_*, coef
+    int64_t nchunks;
+    int W;                      // ranks
+    int rank;                   // this process's rank, or -1: emulation (all ranks in one launch,
+                                // rank = blockIdx.x / nb)
+    int nb;                     // CTAs per rank
+    PeerRank R[kMaxParts];      // every rank's buffers as addressed from this process
+};
+// variant (piece capacity) and co-resident CTAs of k_pcg for a level
+int pcg_resident_blocks(double nnz, double rows);
+void pcg_launch(const PeerCGArgs &a, cudaStream_t st);
 void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches);
 void spmv_csr(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *val,
               const double *v, double *y, cudaStream_t st, int *launches);

@@ -6,27 +6,23 @@
 // close).  Per level:
 //   1. every lane computes its 3^d candidate cells (clamped, as
 //      for_each_range); the warp reduces them to a box of cells;
-//   2. the box is a set of "columns" (3-D: (ix, iy); 2-D: ix) whose cells
-//      along the last axis are contiguous in key order, so each column is ONE
-//      contiguous range of points: the columns' cell_start rows are staged in
-//      shared memory, then the FP32 prefilter records of every column are
-//      bulk-copied (cp.async, 16 B per lane) into a per-warp buffer;
-//   3. candidates are tested from shared memory, either
-//        broadcast -- every lane tests every staged record (one LDS.128
-//                     serves the warp; no divergence), when the box holds at
-//                     most MSK_WS_BRATIO x the largest per-lane candidate
-//                     count (coarse source levels: targets share cells), or
-//        per lane  -- each lane tests its own 3^(d-1) column ranges (fine
-//                     levels: the warp's targets span many cells);
-//   4. survivors of the conservative FP32 prefilter go to a per-lane hit list
-//      in shared memory; flush() runs the exact FP64 test (reading C-4) and
-//      the kernel evaluation on them (caller-supplied).
+//   2. if the box has at most LevelView::bcells cells (default 2.5 x 3^d) (the targets share cells:
+//      every coarser source level), it is a few "columns" (3-D: (ix, iy);
+//      2-D: ix) whose cells along the last axis are contiguous in key order,
+//      i.e. ONE contiguous range of points each: the columns' cell_start rows
+//      are staged in shared memory, then their FP32 prefilter records are
+//      copied (cp.async, 16 B per lane) into a per-warp buffer, and EVERY lane
+//      tests EVERY staged record (one broadcast LDS.128 serves the warp; the
+//      loop is warp-uniform, so hit-list flushes are warp-uniform too);
+//   3. otherwise (fine source levels: the targets span many cells) every lane
+//      enumerates its own 3^d cells from global memory (through L1);
+//   4. survivors of the conservative FP32 prefilter go to a per-lane hit list;
+//      flush() runs the exact FP64 test (reading C-4) and the kernel
+//      evaluation on them (caller-supplied).
 // Candidates are visited in ascending spatial index in both modes (columns in
 // key order, ranges ascending), and the broadcast mode's extra candidates all
 // fail the exact test, so the hits and their order -- and the sums -- are
 // those of the per-thread enumeration (for_each_range): bit-identical.
-// A box that does not fit (too many columns, cells or records) falls back to
-// the per-lane enumeration straight from global memory.
 #pragma once
 #include <climits>
 
@@ -38,24 +34,20 @@ namespace msk {
 namespace wscan {
 
 #ifndef MSK_WS_CAP
-#define MSK_WS_CAP 384    // staged FP32 records per warp
+#define MSK_WS_CAP 256    // staged FP32 records per warp
 #endif
 #ifndef MSK_WS_HM
-#define MSK_WS_HM 24      // hit-list capacity per lane (flushed when full)
+#define MSK_WS_HM 40      // hit-list capacity per lane (flushed when full)
 #endif
 #ifndef MSK_WS_CSCAP
-#define MSK_WS_CSCAP 256  // staged cell_start entries per warp
-#endif
-#ifndef MSK_WS_BRATIO
-#define MSK_WS_BRATIO 1.8f
+#define MSK_WS_CSCAP 128  // staged cell_start entries per warp
 #endif
 constexpr int CAP = MSK_WS_CAP, HM = MSK_WS_HM, CSCAP = MSK_WS_CSCAP, MAXCOL = 32;
 
 struct __align__(16) WarpSmem {
-    float4 rec[CAP];      // staged prefilter records, columns concatenated
-    int hl[HM * 32];      // hit lists, [slot][lane] (conflict-free)
-    int cs[CSCAP];        // cell_start rows of the box columns, (nz + 1) per column
-    int colgb[MAXCOL];    // first global point index of each column
+    float4 rec[CAP];        // staged prefilter records, columns concatenated
+    int cs[CSCAP];          // cell_start rows of the box columns, (nz + 1) per column
+    int colgb[MAXCOL];      // first global point index of each column
     int colfo[MAXCOL + 1];  // offset of each column in rec[] (+ total)
 };
 
@@ -72,12 +64,17 @@ __device__ __forceinline__ bool pre(const float *xf, const float4 &F, float thr)
 }
 
 // One level for the warp.  x / xf: the lane's target (FP64, FP32 relative to
-// the common origin); on: the lane has a target.  flush(nh): process the
-// lane's hits W.hl[h * 32 + lane], h < nh (ascending global index), in order.
-// Must be called by all 32 lanes (warp-collective).
+// the common origin); on: the lane has a target.  hl: the lane's hit list;
+// flush(nh): process hl[0..nh) (ascending global index) in order.  Must be
+// called by all 32 lanes (warp-collective).
+//
+// Mode by box size: at most L.bcells cells (the warp's targets share
+// cells: coarse source levels) => broadcast from shared memory, flushes
+// warp-uniform (all lanes flush together when any list is nearly full);
+// otherwise every lane enumerates its own 3^d cells from global memory (L1).
 template <int D, class Flush>
 __device__ __forceinline__ void scan_level(const LevelView &L, const double *x, const float *xf, bool on,
-                                           WarpSmem &W, Flush &&flush) {
+                                           WarpSmem &W, int (&hl)[HM], Flush &&flush) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const float thr = L.fthr;
@@ -109,31 +106,8 @@ __device__ __forceinline__ void scan_level(const LevelView &L, const double *x, 
     const int zl = b0[D - 1];
     const int64_t nz = (int64_t)b1[D - 1] - zl + 1;
     int nh = 0;
-    auto append = [&](int j) {
-        if (nh == HM) {
-            flush(nh);
-            nh = 0;
-        }
-        W.hl[nh * 32 + lane] = j;
-        ++nh;
-    };
-    // candidates [s0, s1) of the staged buffer; global index = s + gadd
-    auto scan_range = [&](int s0, int s1, int gadd, bool ok) {
-        int s = s0;
-        for (; s + 3 < s1; s += 4) {
-            const float4 F0 = W.rec[s], F1 = W.rec[s + 1], F2 = W.rec[s + 2], F3 = W.rec[s + 3];
-            const bool h0 = ok && pre(xf, F0, thr), h1 = ok && pre(xf, F1, thr);
-            const bool h2 = ok && pre(xf, F2, thr), h3 = ok && pre(xf, F3, thr);
-            if (h0) append(s + gadd);
-            if (h1) append(s + 1 + gadd);
-            if (h2) append(s + 2 + gadd);
-            if (h3) append(s + 3 + gadd);
-        }
-        for (; s < s1; ++s)
-            if (ok && pre(xf, W.rec[s], thr)) append(s + gadd);
-    };
-    bool staged = nx * ny <= MAXCOL && nx * ny * (nz + 1) <= CSCAP;  // warp-uniform
-    if (staged) {
+    bool bc = nx * ny <= MAXCOL && nx * ny * (nz + 1) <= CSCAP && (float)(nx * ny * nz) <= L.bcells;
+    if (bc) {  // warp-uniform
         const int ncol = (int)(nx * ny), w = (int)nz + 1, nyi = (int)ny;
         __syncwarp();  // the previous level's readers of W are done
         for (int t = lane; t < ncol * w; t += 32) {
@@ -141,6 +115,7 @@ __device__ __forceinline__ void scan_level(const LevelView &L, const double *x, 
             const int64_t ix = b0[0] + ci / nyi;
             const int64_t key = D == 3 ? (ix * L.g.dim[1] + (b0[1] + ci % nyi)) * L.g.dim[2] + zl + z
                                        : ix * L.g.dim[1] + zl + z;
+            MSK_DASSERT(t < CSCAP && key >= 0 && key <= L.g.ncells);
             W.cs[t] = L.cell_start[key];
         }
         __syncwarp();
@@ -161,55 +136,72 @@ __device__ __forceinline__ void scan_level(const LevelView &L, const double *x, 
             W.colfo[lane] = inc - len;
         }
         if (lane == 0) W.colfo[ncol] = T;
-        staged = T <= CAP;
-        if (staged) {
-            // largest per-lane candidate count decides the mode
-            int own = 0;
-            if (valid) {
-                const int zlo = lo[D - 1] - zl, zhi = hi[D - 1] - zl + 1;
-                for (int ix = lo[0]; ix <= hi[0]; ++ix)
-                    for (int iy = (D == 3 ? lo[1] : 0); iy <= (D == 3 ? hi[1] : 0); ++iy) {
-                        const int ci = (ix - b0[0]) * nyi + (D == 3 ? iy - b0[1] : 0);
-                        own += W.cs[ci * w + zhi] - W.cs[ci * w + zlo];
-                    }
-            }
-            const int ownmax = __reduce_max_sync(FULL, own);
-            const bool bcast = (float)T <= MSK_WS_BRATIO * (float)ownmax;
+        bc = T <= CAP;
+        if (bc) {
             __syncwarp();
             for (int ci = 0; ci < ncol; ++ci) {
                 const int g0 = W.colgb[ci], f0 = W.colfo[ci], n0 = W.colfo[ci + 1] - f0;
-                for (int t = lane; t < n0; t += 32) cp_async16(&W.rec[f0 + t], &L.frec[g0 + t]);
+                for (int t = lane; t < n0; t += 32) {
+                    MSK_DASSERT(f0 + t < CAP && g0 + t >= 0 && g0 + t < L.n);
+                    cp_async16(&W.rec[f0 + t], &L.frec[g0 + t]);
+                }
             }
             cp_async_wait_all();
             __syncwarp();
-            if (bcast) {
-                for (int ci = 0; ci < ncol; ++ci) {
-                    const int f0 = W.colfo[ci], f1 = W.colfo[ci + 1];
-                    scan_range(f0, f1, W.colgb[ci] - f0, valid);
-                }
-            } else if (valid) {
-                const int zlo = lo[D - 1] - zl, zhi = hi[D - 1] - zl + 1;
-                for (int ix = lo[0]; ix <= hi[0]; ++ix)
-                    for (int iy = (D == 3 ? lo[1] : 0); iy <= (D == 3 ? hi[1] : 0); ++iy) {
-                        const int ci = (ix - b0[0]) * nyi + (D == 3 ? iy - b0[1] : 0);
-                        const int base = W.colfo[ci] - W.colgb[ci];
-                        scan_range(W.cs[ci * w + zlo] + base, W.cs[ci * w + zhi] + base, -base, true);
+            // every lane tests every staged record (one broadcast LDS.128 per
+            // record for the warp), in key order = ascending global index
+            for (int ci = 0; ci < ncol; ++ci) {
+                const int f1 = W.colfo[ci + 1], gadd = W.colgb[ci] - W.colfo[ci];
+                int s = W.colfo[ci];
+                for (; s + 3 < f1; s += 4) {
+                    if (__any_sync(FULL, nh + 4 > HM)) {  // warp-uniform flush
+                        if (nh) flush(nh);
+                        nh = 0;
                     }
+                    const float4 F0 = W.rec[s], F1 = W.rec[s + 1], F2 = W.rec[s + 2], F3 = W.rec[s + 3];
+                    const bool h0 = valid && pre(xf, F0, thr), h1 = valid && pre(xf, F1, thr);
+                    const bool h2 = valid && pre(xf, F2, thr), h3 = valid && pre(xf, F3, thr);
+                    if (h0) hl[nh++] = s + gadd;
+                    if (h1) hl[nh++] = s + 1 + gadd;
+                    if (h2) hl[nh++] = s + 2 + gadd;
+                    if (h3) hl[nh++] = s + 3 + gadd;
+                }
+                for (; s < f1; ++s) {
+                    if (__any_sync(FULL, nh + 1 > HM)) {
+                        if (nh) flush(nh);
+                        nh = 0;
+                    }
+                    if (valid && pre(xf, W.rec[s], thr)) hl[nh++] = s + gadd;
+                }
             }
         }
     }
-    if (!staged && valid) {
-        // fallback: the lane's own ranges straight from global memory
+    if (!bc && valid) {
+        // the lane's own 3^d cells straight from global memory (through L1)
         const float4 *__restrict__ frec = L.frec;
         for_each_range<D>(L, x, [&](int b, int e) {
             int j = b;
-            for (; j + 1 < e; j += 2) {
-                const float4 F0 = frec[j], F1 = frec[j + 1];
+            for (; j + 3 < e; j += 4) {
+                const float4 F0 = frec[j], F1 = frec[j + 1], F2 = frec[j + 2], F3 = frec[j + 3];
                 const bool h0 = pre(xf, F0, thr), h1 = pre(xf, F1, thr);
-                if (h0) append(j);
-                if (h1) append(j + 1);
+                const bool h2 = pre(xf, F2, thr), h3 = pre(xf, F3, thr);
+                if (nh + 4 > HM) {
+                    flush(nh);
+                    nh = 0;
+                }
+                if (h0) hl[nh++] = j;
+                if (h1) hl[nh++] = j + 1;
+                if (h2) hl[nh++] = j + 2;
+                if (h3) hl[nh++] = j + 3;
             }
-            if (j < e && pre(xf, frec[j], thr)) append(j);
+            for (; j < e; ++j) {
+                const bool h0 = pre(xf, frec[j], thr);
+                if (nh + 1 > HM) {
+                    flush(nh);
+                    nh = 0;
+                }
+                if (h0) hl[nh++] = j;
+            }
         });
     }
     if (nh) flush(nh);

@@ -1,6 +1,8 @@
 """Partitioned (multi-GPU) path, run as the single-process emulation on one
-GPU: `world` partitions per level, chunk partials all-reduced, r halos
-exchanged between separate partition buffers.
+GPU: `world` partitions per level with separate buffers; chunk partials and r
+halos exchanged either inside one persistent launch over "peer" stores (k_pcg,
+the path of a real multi-GPU job) or by host-driven phase kernels (DESIGN.md
+§Multi-GPU).
 
 Because every partial is formed per chunk exactly as in the single-GPU
 kernel and summed over all chunks in the same order, the partitioned solve
@@ -40,7 +42,13 @@ def _solve(msk, ctx, H, flags, f, x):
 
 @pytest.mark.parametrize("name", list(HIERS))
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_partitioned_equals_single_gpu_bitwise(msk, name, world):
+@pytest.mark.parametrize("path", ["p2p", "phase"])
+def test_partitioned_equals_single_gpu_bitwise(msk, name, world, path, monkeypatch):
+    """path p2p: the whole CG of a partitioned level in one launch over peer
+    memory (k_pcg: partials and r halos stored into the other partitions'
+    buffers, device-side cross-partition barrier); path phase: host-driven phase
+    kernels with the partials summed and the halos copied between launches."""
+    monkeypatch.setenv("MSK_DIST_P2P", "1" if path == "p2p" else "0")
     H = HIERS[name]()
     f = H.f()
     x = uniform_points(5000, H.d, seed=4)

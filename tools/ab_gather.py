@@ -1,5 +1,5 @@
-"""A/B of the matrix-free kernel sums: per-thread (MSK_GATHER_V1=1) against
-the warp-cooperative staged scan (default).  Each variant runs in its own
+"""A/B of the matrix-free kernel sums: per-thread (default) against the
+warp-cooperative staged scan (MSK_GATHER_WARP=1).  Each variant runs in its own
 process (the switch is read once); outputs must be bit-identical.
 
     python tools/ab_gather.py [--config C3] [--mf] [--m-eval 10000000]
@@ -41,7 +41,7 @@ def child(args, out):
             rec["cg"].append(info.t_cg_ms)
             rec["cg_levels"] = list(info.t_cg_level_ms)[:H.L]
     np.savez(out, *[v.cpu().numpy() for v in a], s=s.cpu().numpy())
-    res = {"variant": "v1" if os.environ.get("MSK_GATHER_V1") else "warp", "config": args.config,
+    res = {"variant": "warp" if os.environ.get("MSK_GATHER_WARP") else "v1", "config": args.config,
            "mf": args.mf, "b_products_ms": float(np.median(rec["b"])), "eval_kernel_ms": float(np.median(rec["eval"])),
            "cg_ms": float(np.median(rec["cg"])), "cg_level_ms": rec["cg_levels"],
            "nnz_gather": info.nnz_gather, "nnz_eval": einfo.nnz}
@@ -64,8 +64,9 @@ def main():
     for v1 in (True, False):
         env = dict(os.environ)
         env.pop("MSK_GATHER_V1", None)
-        if v1:
-            env["MSK_GATHER_V1"] = "1"
+        env.pop("MSK_GATHER_WARP", None)
+        if not v1:
+            env["MSK_GATHER_WARP"] = "1"
         out = os.path.join(tmp, f"v{int(v1)}.npz")
         cmd = [sys.executable, __file__, "--config", args.config, "--reps", str(args.reps), "--child", out]
         if args.mf:
