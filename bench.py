@@ -130,6 +130,8 @@ def run_msk(args, rank, world, local_rank):
     patch_R = args.patch_R if args.patch_R is not None else (11.0 if args.config == "C4F" else 0.0)
 
     hflags = msk.MSK_FLAG_MATRIX_FREE if args.matrix_free else 0
+    if world > 1:  # each rank keeps its share of s_L (no all-gather of the 80 MB result)
+        hflags |= msk.MSK_FLAG_OUTPUT_LOCAL
 
     def step(pts, f, xe, alpha, s):
         h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=H.k, flags=hflags)
@@ -282,8 +284,10 @@ def run_msk(args, rank, world, local_rank):
                    "m_eval": int(H.eval_points.shape[0]),
                    "nnz_per_step": nnz_local,
                    "l2": "inputs (274 MB points, 240 MB eval points) larger than the 126 MB L2, plus a 256 MB flush write between steps",
-                   "parallelism": (f"partitioned x{world}: levels >= 2^20 points split in row blocks, NCCL "
-                                   f"halo + chunk-partial all-reduce; smaller levels redundant") if world > 1
+                   "parallelism": (f"partitioned x{world}: large levels split in row blocks, CG of each in one "
+                                   f"k_pcg launch per rank over NVLink peer memory (partials + r halos stored "
+                                   f"into the peers, device-side barrier); smaller levels redundant; s_L "
+                                   f"rank-local (MSK_FLAG_OUTPUT_LOCAL)") if world > 1
                    else "single",
                    "phase_ms": {"create": hinfo.t_create_ms, "assemble": hinfo.t_assemble_ms,
                                 "solve": sinfo.t_total_ms, "solve_cg": sinfo.t_cg_ms,

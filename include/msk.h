@@ -74,9 +74,14 @@ typedef enum {
 #define MSK_FLAG_MATRIX_FREE 2u /* a3 matrix-free: A_l is never stored;
                                    every CG SpMV evaluates Phi on the fly over the level's cell list,
                                    visiting the columns in the stored CSR order, so alpha is
-                                   BIT-IDENTICAL to the assembled solve.  msk_assemble(T > 0),
-                                   the LITERAL schedule and msk_cg_level are MSK_ERR_INVALID /
-                                   MSK_ERR_STATE on such a hierarchy (PRUNED only) */
+                                   BIT-IDENTICAL to the assembled solve (both schedules).
+                                   msk_assemble(T > 0) and msk_cg_level are MSK_ERR_INVALID /
+                                   MSK_ERR_STATE on such a hierarchy */
+
+#define MSK_FLAG_OUTPUT_LOCAL 4u /* distributed context: msk_evaluate writes only the values of this
+                                    rank's share of the (spatially sorted) evaluation points and skips
+                                    their all-gather (perf runs that consume s_L rank-locally); alpha is
+                                    complete either way.  No effect on one GPU or in the emulation */
 
 /* msk_solve schedules */
 #define MSK_SCHED_PRUNED 0u  /* Algorithm 2 with each inner solve t^{(l)} = A_l^{-1} beta^{(l)} done
@@ -188,7 +193,8 @@ MSK_API msk_status msk_halo_plan(int world, int rank, const int64_t *rows, const
  *                the pattern pass when the closest pair lies within delta_l,
  *                else by a widening cell search (a one-point level: delta_l/2).
  *   wendland_k   0, 1 or 2: phi_{d,k} (reading C-3).
- *   flags        MSK_FLAG_NONE, or an OR of MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE.
+ *   flags        MSK_FLAG_NONE, or an OR of MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE,
+ *                MSK_FLAG_OUTPUT_LOCAL.
  * Duplicate points within one level => MSK_ERR_INVALID. */
 MSK_API msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int64_t *n,
                                 const double *const *points, const double *delta,
@@ -278,7 +284,9 @@ MSK_API msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double *x,
  * L = 1 gives 0. */
 MSK_API msk_status msk_m_norm(msk_hierarchy *h, int32_t max_iter, double rel_tol, double cg_tol, double *norm,
                       int32_t *iters);
-/* which = 0: ||M_L||_2 (as msk_m_norm); which = 1: ||M_L - M~_L(T)||_2 with the
+/* which = 0: ||M_L||_2 (as msk_m_norm); which = 2: ||M~_L(T)||_2 of the stored
+ * factor alone (the max(||M||, ||M~||) of the corrected Lemma pert1 bound,
+ * DESIGN.md reading C-22); which = 1: ||M_L - M~_L(T)||_2 with the
  * stored thresholded factor of the last msk_assemble(T > 0) (Figure 2,
  * M - M~ = -(X - X~), X~ applied from the stored CSR and its
  * transpose; MSK_ERR_STATE without a factor).  The transposed product sums a

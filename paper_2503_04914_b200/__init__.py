@@ -16,7 +16,7 @@ import weakref
 import numpy as np
 
 from . import _lib
-from ._lib import (EXPORTED, MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE, MSK_SCHED_LITERAL, MSK_SCHED_PRUNED, EvalInfo, HierarchyInfo,
+from ._lib import (EXPORTED, MSK_FLAG_DIST_ALL, MSK_FLAG_MATRIX_FREE, MSK_FLAG_OUTPUT_LOCAL, MSK_SCHED_LITERAL, MSK_SCHED_PRUNED, EvalInfo, HierarchyInfo,
                    MskError, SolveInfo, check, load)
 
 __all__ = ["Context", "Hierarchy", "MskError", "SolveInfo", "HierarchyInfo", "EvalInfo",
@@ -345,6 +345,10 @@ class Hierarchy:
     def m_diff_norm(self, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
         """||M_L - M~_L(T)||_2 (Figure 2) with the stored factor: (norm, iterations)."""
         return msk_m_norm_ex(self.handle, 1, max_iter, rel_tol, cg_tol)
+
+    def m_tilde_norm(self, max_iter=500, rel_tol=1e-9, cg_tol=1e-13):
+        """||M~_L(T)||_2 of the stored factor alone: (norm, iterations)."""
+        return msk_m_norm_ex(self.handle, 2, max_iter, rel_tol, cg_tol)
 
     def evaluate_multi(self, x):
         x = _f64(x)

@@ -114,6 +114,7 @@ EXPORTED = ["msk_ctx_create", "msk_ctx_destroy", "msk_hierarchy_create", "msk_hi
             "msk_nccl_unique_id", "msk_partition_rows", "msk_halo_plan", "msk_last_error", "msk_version"]
 MSK_FLAG_DIST_ALL = 1
 MSK_FLAG_MATRIX_FREE = 2
+MSK_FLAG_OUTPUT_LOCAL = 4
 
 
 def check(status: int) -> None:

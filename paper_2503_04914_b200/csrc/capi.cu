@@ -128,7 +128,8 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
         require(d == 2 || d == 3, "msk_hierarchy_create: d must be 2 or 3");
         require(L >= 1 && L <= kMaxLevels, "msk_hierarchy_create: L must be in 1..16");
         require(wendland_k >= 0 && wendland_k <= 2, "msk_hierarchy_create: k must be 0, 1 or 2");
-        require((flags & ~(MSK_FLAG_DIST_ALL | MSK_FLAG_MATRIX_FREE)) == 0, "msk_hierarchy_create: unknown flags");
+        require((flags & ~(MSK_FLAG_DIST_ALL | MSK_FLAG_MATRIX_FREE | MSK_FLAG_OUTPUT_LOCAL)) == 0,
+                "msk_hierarchy_create: unknown flags");
         for (int l = 0; l < L; ++l) {
             require(n[l] >= 1 && n[l] < (1ll << 31) - 1, "msk_hierarchy_create: n[l] out of range");
             require(points[l] != nullptr, "msk_hierarchy_create: NULL points");

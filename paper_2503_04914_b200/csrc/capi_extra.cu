@@ -219,8 +219,8 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
                                     double cg_tol, double *norm, int32_t *iters) {
     API_BEGIN
     require(h && norm, "msk_m_norm: NULL argument");
-    require(which == 0 || which == 1, "msk_m_norm: which must be 0 (M) or 1 (M - M~(T))");
-    if (which == 1 && !(h->T > 0.0))
+    require(which >= 0 && which <= 2, "msk_m_norm: which must be 0 (M), 1 (M - M~(T)) or 2 (M~(T))");
+    if (which >= 1 && !(h->T > 0.0))
         throw Error(MSK_ERR_STATE, "msk_m_norm: M - M~(T) needs the thresholded factor (msk_assemble with T > 0)");
     require(max_iter >= 1 && rel_tol > 0.0 && cg_tol > 0.0 && cg_tol < 1.0, "msk_m_norm: bad arguments");
     if (!h->assembled) throw Error(MSK_ERR_STATE, "msk_m_norm: call msk_assemble first");
@@ -243,7 +243,7 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
     int32_t *crow = nullptr, *ccol = nullptr;
     double *nv = nullptr;
     const int64_t ncols = h->off[L - 1];
-    if (which == 1) {
+    if (which >= 1) {
         cptr = dalloc<int64_t>((size_t)(ncols + 1), st);
         cpos = dalloc<int64_t>((size_t)h->tnnz + 1, st);
         crow = dalloc<int32_t>((size_t)h->tnnz + 1, st);
@@ -266,11 +266,12 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
     double sigma = 0.0;
     int it = 0;
     for (; it < max_iter; ++it) {
-        // u = M v
-        solve_coarse(v, t);
-        MSK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * (size_t)h->lev[0].n, st));
-        for (int l = 0; l + 1 < L; ++l) h->pack(l, t + h->off[l], nullptr);
-        for (int k = 1; k < L; ++k) {
+        // u = M v  (which = 2: u = M~ v = -X~ v only)
+        if (which == 2) MSK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * (size_t)N, st));
+        else solve_coarse(v, t);
+        if (which != 2) MSK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * (size_t)h->lev[0].n, st));
+        for (int l = 0; l + 1 < L && which != 2; ++l) h->pack(l, t + h->off[l], nullptr);
+        for (int k = 1; k < L && which != 2; ++k) {
             GatherArgs ga{};
             ga.d = h->d;
             ga.k = h->k;
@@ -282,6 +283,10 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
             ga.out = u + h->off[k];
             gather(ga, st, nullptr);
         }
+        if (which == 2) {  // u = 0 - X~ v
+            thresh_residual(h->off[1], N, h->trow_ptr, h->tcol, h->tval, u, v, u, st, nullptr, h->tbucket,
+                            h->tmax_active);
+        }
         if (which == 1) {  // u += X~ v  (thresh_residual: out = base - sum val * (-v))
             MSK_CUDA(cudaMemcpyAsync(nv, v, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, st));
             dev_scale(nv, -1.0, N, st);
@@ -290,7 +295,7 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
         }
         const double s_new = sqrt(dev_dot(u, u, N, scratch, st));
         // w = M^T u = -A^{-1} (B^T u) on the coarse levels, 0 on the finest
-        for (int l = 0; l + 1 < L; ++l) {
+        for (int l = 0; l + 1 < L && which != 2; ++l) {
             GatherTArgs gt{};
             gt.d = h->d;
             gt.k = h->k;
@@ -310,9 +315,10 @@ extern "C" msk_status msk_m_norm_ex(msk_hierarchy *h, int32_t which, int32_t max
             gt.out = t + h->off[l];
             gather_t(gt, st, nullptr);
         }
-        solve_coarse(t, w);
+        if (which == 2) MSK_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * (size_t)N, st));
+        else solve_coarse(t, w);
         MSK_CUDA(cudaMemsetAsync(w + h->off[L - 1], 0, sizeof(double) * (size_t)h->lev[L - 1].n, st));
-        if (which == 1)  // w += X~^T u
+        if (which >= 1)  // w += X~^T u  (which = 2: the sign of M~^T is immaterial to the norm)
             csc_spmv_add(ncols, cptr, cpos, crow, h->tval, u, w, st, h->tbucket, h->tmax_active);
         const double wn = sqrt(dev_dot(w, w, N, scratch, st));
         const bool done = it > 0 && fabs(s_new - sigma) <= rel_tol * s_new;

@@ -119,23 +119,38 @@ bool peer_setup(msk_hierarchy *h, int l, int64_t nch) {
     ck(cudaMalloc((void **)&M.part, sizeof(double) * (size_t)(3 * nch)));
     ck(cudaMalloc((void **)&M.alpha, sizeof(double) * (size_t)n));
     ck(cudaMalloc((void **)&M.cnt, sizeof(unsigned long long) * 3));
-    constexpr int NB = 4;  // handles per rank
-    std::vector<cudaIpcMemHandle_t> mine(NB);
-    memset(mine.data(), 0, sizeof(cudaIpcMemHandle_t) * NB);
+    constexpr int NB = 4;  // handles per rank, then the device UUID
+    struct Blob {
+        cudaIpcMemHandle_t hd[NB];
+        unsigned char uuid[16];
+    };
+    Blob mine;
+    memset(&mine, 0, sizeof mine);
     if (!fail) {
         ck(cudaMemset(M.cnt, 0, sizeof(unsigned long long) * 3));
-        ck(cudaIpcGetMemHandle(&mine[0], M.r));
-        ck(cudaIpcGetMemHandle(&mine[1], M.part));
-        ck(cudaIpcGetMemHandle(&mine[2], M.alpha));
-        ck(cudaIpcGetMemHandle(&mine[3], M.cnt));
+        ck(cudaIpcGetMemHandle(&mine.hd[0], M.r));
+        ck(cudaIpcGetMemHandle(&mine.hd[1], M.part));
+        ck(cudaIpcGetMemHandle(&mine.hd[2], M.alpha));
+        ck(cudaIpcGetMemHandle(&mine.hd[3], M.cnt));
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, h->ctx->device));
+        if (!fail) memcpy(mine.uuid, &prop.uuid, 16);
     }
-    const size_t hb = sizeof(cudaIpcMemHandle_t) * NB;
+    const size_t hb = sizeof(Blob);
     unsigned char *dh = dalloc<unsigned char>(hb * (size_t)(W + 1), st);
-    MSK_CUDA(cudaMemcpyAsync(dh + hb * W, mine.data(), hb, cudaMemcpyHostToDevice, st));
+    MSK_CUDA(cudaMemcpyAsync(dh + hb * W, &mine, hb, cudaMemcpyHostToDevice, st));
     MSK_NCCL(nccl_api()->AllGather(dh + hb * W, dh, hb, ncclUint8, h->ctx->comm, st));
-    std::vector<cudaIpcMemHandle_t> all((size_t)(NB * W));
-    MSK_CUDA(cudaMemcpyAsync(all.data(), dh, hb * W, cudaMemcpyDeviceToHost, st));
+    std::vector<Blob> blobs((size_t)W);
+    MSK_CUDA(cudaMemcpyAsync(blobs.data(), dh, hb * W, cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaStreamSynchronize(st));
+    // ranks that share a device (threads as ranks, several processes on one
+    // GPU) must not run kernels that wait on each other: phase path instead
+    for (int a = 0; a < W && !fail; ++a)
+        for (int b = a + 1; b < W; ++b)
+            if (memcmp(blobs[a].uuid, blobs[b].uuid, 16) == 0) fail = 1;
+    std::vector<cudaIpcMemHandle_t> all((size_t)(NB * W));
+    for (int w = 0; w < W; ++w)
+        for (int k = 0; k < NB; ++k) all[(size_t)(NB * w + k)] = blobs[w].hd[k];
     M.pr.assign(W, nullptr); M.ppart.assign(W, nullptr); M.palpha.assign(W, nullptr); M.pcnt.assign(W, nullptr);
     for (int w = 0; w < W && !fail; ++w) {
         if (w == me) {
@@ -160,6 +175,24 @@ bool peer_setup(msk_hierarchy *h, int l, int64_t nch) {
     dfree(dh, st);
     M.ok = tot == 0;
     return M.ok;
+}
+// v (spatial order) complete on every rank from each rank's rows [rows[r],
+// rows[r+1]): one in-place all-gather of equal blocks (the largest share),
+// then the blocks moved to their rows -- instead of a zero-filled all-reduce
+void allgather_rows(msk_hierarchy *h, double *v, const std::vector<int64_t> &rows, cudaStream_t st) {
+    const int W = h->ctx->world, me = h->ctx->rank;
+    int64_t smax = 1;
+    for (int r = 0; r < W; ++r) smax = std::max(smax, rows[r + 1] - rows[r]);
+    double *buf = dalloc<double>((size_t)(smax * W), st);
+    if (rows[me + 1] > rows[me])
+        MSK_CUDA(cudaMemcpyAsync(buf + me * smax, v + rows[me], sizeof(double) * (size_t)(rows[me + 1] - rows[me]),
+                                 cudaMemcpyDeviceToDevice, st));
+    MSK_NCCL(nccl_api()->AllGather(buf + me * smax, buf, (size_t)smax, ncclFloat64, h->ctx->comm, st));
+    for (int r = 0; r < W; ++r)
+        if (r != me && rows[r + 1] > rows[r])
+            MSK_CUDA(cudaMemcpyAsync(v + rows[r], buf + r * smax, sizeof(double) * (size_t)(rows[r + 1] - rows[r]),
+                                     cudaMemcpyDeviceToDevice, st));
+    dfree(buf, st);
 }
 }  // namespace
 
@@ -260,6 +293,26 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         ga_t.back()->stop();
     };
 
+    // B products for rows [r0, r1) of target level k only (a partitioned level's owned rows)
+    auto b_products_rows = [&](int k, double *const *coef_spatial, double *out_spatial, int64_t r0, int64_t r1) {
+        GatherArgs ga{};
+        ga.d = h->d;
+        ga.k = h->k;
+        ga.nt = r1 - r0;
+        for (int a = 0; a < h->d; ++a) ga.tx[a] = h->lev[k].xs + (size_t)a * h->lev[k].n + r0;
+        ga.nlev = k;
+        for (int l = 0; l < k; ++l) ga.lev[l] = h->view(l, coef_spatial[l]);
+        ga.base = fd[k].ptr;
+        ga.base_perm = h->lev[k].perm + r0;
+        ga.sign = -1.0;
+        ga.out = out_spatial + r0;
+        ga.out_perm = nullptr;
+        ga.hits = d_hits;
+        time_ga();
+        gather(ga, st, &launches);
+        ga_t.back()->stop();
+    };
+
     ttot.start();
     std::vector<double *> alpha_sp(L), t_sp(L);
     for (int l = 0; l < L; ++l) {
@@ -271,7 +324,13 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
     // beta on the owned rows, then the CG as phase kernels with all-reduced
     // chunk partials and halo exchange of r; alpha assembled on every rank.
     // beta_ready: beta^(l) is already in ws_beta(l) (thresholded factor, a7)
-    auto dist_level = [&](int l, double tl, bool beta_ready) {
+    // slot: stats slot (LITERAL: one per sweep + the final solves); out: the
+    // complete solution vector (spatial order, every rank); to_caller: also
+    // write it to the caller's alpha^(l)
+    auto dist_level = [&](int l, double tl, bool beta_ready, int slot = 0, double *out = nullptr,
+                          bool to_caller = true) {
+        if (!out) out = alpha_sp[l];
+        const int si = slot * L + l;
         auto &Dd = h->dist[l];
         LevelData &D = h->lev[l];
         const int64_t n = D.n;
@@ -293,6 +352,17 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         std::vector<double *> owned_alloc;
         double *recv = dalloc<double>((size_t)nch, st);
         DistCGScalars *sc = dalloc<DistCGScalars>((size_t)np, st);
+        // real ranks: chunk partials are all-gathered, each rank's owned chunks as
+        // one block of gcmax (the largest owned count) -- no zero-filled arrays
+        int64_t gcmax = 0;
+        std::vector<int64_t> gc0;
+        if (part && !emu) {
+            const int64_t cpr = (int64_t)CH * 256;
+            for (int w = 0; w <= W; ++w) gc0.push_back(w < W ? Dd.rows[w] / cpr : nch);
+            for (int w = 0; w < W; ++w) gcmax = std::max(gcmax, gc0[w + 1] - gc0[w]);
+            gcmax = std::max<int64_t>(gcmax, 1);
+        }
+        double *gbuf = part && !emu ? dalloc<double>((size_t)(gcmax * W), st) : nullptr;
         for (int i = 0; i < np; ++i) {
             if (emu) {
                 double *blk = dalloc<double>((size_t)(4 * n), st);
@@ -302,7 +372,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 X[i] = h->ws_t(l); R[i] = h->ws_r(l); Pv[i] = h->ws_p(l); Q[i] = h->ws_q(l);
             }
             send[i] = dalloc<double>((size_t)nch, st);
-            MSK_CUDA(cudaMemsetAsync(send[i], 0, sizeof(double) * (size_t)nch, st));
+            if (!gbuf) MSK_CUDA(cudaMemsetAsync(send[i], 0, sizeof(double) * (size_t)nch, st));
         }
         // beta^(l) on the owned rows (B products of the coarser, complete levels)
         if (l > 0 && !beta_ready) {
@@ -343,8 +413,16 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             A.nchunks = nch;
             A.part_send = send[i];
             A.part_recv = part ? recv : send[i];  // one partition: nothing to reduce
+            if (gbuf) {  // chunk c of this rank -> gbuf[rank * gcmax + c - c0]
+                const int me = h->ctx->rank;
+                A.part_send = gbuf + me * gcmax - gc0[me];
+                A.part_recv = gbuf;
+                A.gw = W;
+                A.gcmax = gcmax;
+                for (int w = 0; w <= W; ++w) A.gc0[w] = gc0[w];
+            }
             A.sc = sc + i;
-            if (i == 0) set_coef(A.L, l);
+            if (i == 0) set_coef(A.L, si);
         }
         auto allreduce = [&]() {
             if (!part) return;
@@ -352,8 +430,9 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 DistPtrs ptrs{};
                 for (int i = 0; i < np; ++i) ptrs.p[i] = send[i];
                 sum_arrays(np, ptrs, recv, nch, st);
-            } else {
-                MSK_NCCL(nccl_api()->AllReduce(send[0], recv, (size_t)nch, ncclFloat64, ncclSum, h->ctx->comm, st));
+            } else {  // in place: this rank's block is already at rank * gcmax
+                MSK_NCCL(nccl_api()->AllGather(gbuf + h->ctx->rank * gcmax, gbuf, (size_t)gcmax, ncclFloat64,
+                                               h->ctx->comm, st));
             }
         };
         // halo plans (msk_halo_plan): per local partition, send/recv row ranges per peer
@@ -391,9 +470,9 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             const auto &P = Dd.local[0];
             PeerCGArgs pa{};
             pa.L = args[0].L;
-            pa.L.out_iters = d_it + l;
-            pa.L.out_rr = d_rr + 2 * l;
-            pa.L.out_status = d_stat + l;
+            pa.L.out_iters = d_it + si;
+            pa.L.out_rr = d_rr + 2 * si;
+            pa.L.out_status = d_stat + si;
             pa.L.nnz = D.nnz;
             pa.nchunks = nch;
             pa.W = W;
@@ -418,15 +497,26 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                     pr.row_ptr = P.rp - P.lo; pr.col = P.col; pr.val = P.val;
                 }
             }
+            for (int w = 0; w < W; ++w) {  // rows of rank w that another rank reads
+                int64_t a = Dd.rows[w + 1], b = Dd.rows[w];
+                for (int v = 0; v < W; ++v) {
+                    if (v == w) continue;
+                    const int64_t s0 = std::max(Dd.rows[w], Dd.hlo[v]), s1 = std::min(Dd.rows[w + 1], Dd.hhi[v]);
+                    if (s0 < s1) { a = std::min(a, s0); b = std::max(b, s1); }
+                }
+                pa.R[w].slo = a;
+                pa.R[w].shi = b;
+            }
             time_cg(l);
             pcg_launch(pa, st);
             launches += 1;
             cg_t.back()->stop();
-            MSK_CUDA(cudaMemcpyAsync(alpha_sp[l], M.alpha, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
-            permute_scatter(n, alpha_sp[l], D.perm, ad[l].ptr, st, &launches);
+            MSK_CUDA(cudaMemcpyAsync(out, M.alpha, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+            if (to_caller) permute_scatter(n, out, D.perm, ad[l].ptr, st, &launches);
             for (double *p : send) dfree(p, st);
             dfree(recv, st);
             dfree(sc, st);
+            dfree(gbuf, st);
             return;
         }
         if (p2p && emu) {
@@ -440,9 +530,9 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             PeerCGArgs pa{};
             pa.L = args[0].L;
             pa.L.x = pa.L.r = pa.L.p = pa.L.q = nullptr;
-            pa.L.out_iters = d_it + l;
-            pa.L.out_rr = d_rr + 2 * l;
-            pa.L.out_status = d_stat + l;
+            pa.L.out_iters = d_it + si;
+            pa.L.out_rr = d_rr + 2 * si;
+            pa.L.out_status = d_stat + si;
             pa.L.nnz = D.nnz;
             pa.nchunks = nch;
             pa.W = np;
@@ -456,7 +546,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 pr.p = Pv[i];
                 pr.q = Q[i];
                 pr.part = pbuf + (size_t)(3 * nch) * i;
-                pr.alpha = alpha_sp[l];  // every partition pushes its owned rows into the one result
+                pr.alpha = out;  // every partition pushes its owned rows into the one result
                 pr.xcnt = cnt + 3 * i;
                 pr.nbar = cnt + 3 * i + 1;
                 pr.gbar = cnt + 3 * i + 2;
@@ -468,13 +558,23 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 pr.hlo = P.hlo;
                 pr.hhi = P.hhi;
             }
+            for (int i = 0; i < np; ++i) {  // rows of partition i that another partition reads
+                int64_t a = parts[i].hi, b = parts[i].lo;
+                for (int j = 0; j < np; ++j) {
+                    if (j == i) continue;
+                    const int64_t s0 = std::max(parts[i].lo, parts[j].hlo), s1 = std::min(parts[i].hi, parts[j].hhi);
+                    if (s0 < s1) { a = std::min(a, s0); b = std::max(b, s1); }
+                }
+                pa.R[i].slo = a;
+                pa.R[i].shi = b;
+            }
             time_cg(l);
             pcg_launch(pa, st);
             launches += 1;
             cg_t.back()->stop();
             dfree(pbuf, st);
             dfree(cnt, st);
-            permute_scatter(n, alpha_sp[l], D.perm, ad[l].ptr, st, &launches);
+            if (to_caller) permute_scatter(n, out, D.perm, ad[l].ptr, st, &launches);
             for (double *p : owned_alloc) dfree(p, st);
             for (double *p : send) dfree(p, st);
             dfree(recv, st);
@@ -513,35 +613,34 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         cg_t.back()->stop();
         // alpha^(l) complete on every rank (spatial order), then caller order
         if (!part) {
-            MSK_CUDA(cudaMemcpyAsync(alpha_sp[l], X[0], sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+            if (out != X[0])
+                MSK_CUDA(cudaMemcpyAsync(out, X[0], sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
         } else if (emu) {
             for (int i = 0; i < np; ++i) {
                 const auto &P = parts[i];
-                MSK_CUDA(cudaMemcpyAsync(alpha_sp[l] + P.lo, X[i] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
+                MSK_CUDA(cudaMemcpyAsync(out + P.lo, X[i] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
                                          cudaMemcpyDeviceToDevice, st));
             }
         } else {
             const auto &P = Dd.local[0];
-            double *tmp = Q[0];
-            MSK_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * (size_t)n, st));
-            MSK_CUDA(cudaMemcpyAsync(tmp + P.lo, X[0] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
-                                     cudaMemcpyDeviceToDevice, st));
-            MSK_NCCL(nccl_api()->AllReduce(tmp, alpha_sp[l], (size_t)n, ncclFloat64, ncclSum, h->ctx->comm, st));
+            if (out != X[0])
+                MSK_CUDA(cudaMemcpyAsync(out + P.lo, X[0] + P.lo, sizeof(double) * (size_t)(P.hi - P.lo),
+                                         cudaMemcpyDeviceToDevice, st));
+            allgather_rows(h, out, Dd.rows, st);
         }
-        permute_scatter(n, alpha_sp[l], D.perm, ad[l].ptr, st, &launches);
-        MSK_CUDA(cudaMemcpyAsync(d_it + l, &sc->it, sizeof(int), cudaMemcpyDeviceToDevice, st));
-        MSK_CUDA(cudaMemcpyAsync(d_stat + l, &sc->status, sizeof(int), cudaMemcpyDeviceToDevice, st));
-        MSK_CUDA(cudaMemcpyAsync(d_rr + 2 * l, &sc->rr, sizeof(double), cudaMemcpyDeviceToDevice, st));
-        MSK_CUDA(cudaMemcpyAsync(d_rr + 2 * l + 1, &sc->bb, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        if (to_caller) permute_scatter(n, out, D.perm, ad[l].ptr, st, &launches);
+        MSK_CUDA(cudaMemcpyAsync(d_it + si, &sc->it, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        MSK_CUDA(cudaMemcpyAsync(d_stat + si, &sc->status, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        MSK_CUDA(cudaMemcpyAsync(d_rr + 2 * si, &sc->rr, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        MSK_CUDA(cudaMemcpyAsync(d_rr + 2 * si + 1, &sc->bb, sizeof(double), cudaMemcpyDeviceToDevice, st));
         for (double *p : owned_alloc) dfree(p, st);
         for (double *p : send) dfree(p, st);
         dfree(recv, st);
         dfree(sc, st);
+        dfree(gbuf, st);
     };
     bool any_dist = false;
     for (int l = 0; l < L; ++l) any_dist = any_dist || h->dist[l].on;
-    require(!any_dist || schedule == MSK_SCHED_PRUNED, "msk_solve: a distributed solve uses the PRUNED schedule");
-    require(!mf || schedule == MSK_SCHED_PRUNED, "msk_solve: a matrix-free hierarchy uses the PRUNED schedule");
 
     const bool thresholded = h->T > 0.0;
     if (thresholded || schedule != MSK_SCHED_PRUNED)
@@ -571,16 +670,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 for (const auto &P : Dk.local)
                     thresh_residual(h->off[k] + P.lo, h->off[k] + P.hi, h->trow_ptr, h->tcol, h->tval, beta, beta,
                                     beta, st, &launches, h->tbucket, h->tmax_active);
-                if (!h->ctx->emulated) {
-                    const int64_t nk = h->lev[k].n;
-                    const auto &P = Dk.local[0];
-                    double *tmp = h->ws_t(k);
-                    MSK_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * (size_t)nk, st));
-                    MSK_CUDA(cudaMemcpyAsync(tmp + P.lo, beta + h->off[k] + P.lo,
-                                             sizeof(double) * (size_t)(P.hi - P.lo), cudaMemcpyDeviceToDevice, st));
-                    MSK_NCCL(nccl_api()->AllReduce(tmp, beta + h->off[k], (size_t)nk, ncclFloat64, ncclSum,
-                                                   h->ctx->comm, st));
-                }
+                if (!h->ctx->emulated) allgather_rows(h, beta + h->off[k], Dk.rows, st);
             }
             ga_t.back()->stop();
         } else {
@@ -656,26 +746,45 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             if (L > 1) {
                 std::vector<CGLevelArgs> a;
                 for (int l = 0; l + 1 < L; ++l) {
+                    if (h->dist[l].on || mf) continue;  // below
                     a.push_back(cg_args(h, l, inner_tol, max_iter, h->ws_beta(l), nullptr, t_sp[l], nullptr,
                                         d_it + sweep * L + l, d_rr + 2 * (sweep * L + l), d_stat + sweep * L + l));
                     set_coef(a.back(), sweep * L + l);
                 }
-                time_cg(-1);
-                cg_batched(a.data(), (int)a.size(), st, &launches);
-                cg_t.back()->stop();
+                if (!a.empty()) {
+                    time_cg(-1);
+                    cg_batched(a.data(), (int)a.size(), st, &launches);
+                    cg_t.back()->stop();
+                }
+                // partitioned inner levels (distributed context): the partitioned CG,
+                // t^(l) complete on every rank afterwards; matrix-free levels: the
+                // phase kernels with k_mf_spmv
+                for (int l = 0; l + 1 < L; ++l)
+                    if (h->dist[l].on || mf) dist_level(l, inner_tol, true, sweep, t_sp[l], false);
                 for (int l = 0; l + 1 < L; ++l) h->pack(l, t_sp[l], &launches);
-                for (int k = 1; k < L; ++k) b_products(k, t_sp.data(), h->ws_beta(k));
+                for (int k = 1; k < L; ++k) {
+                    const auto &Dk = h->dist[k];
+                    if (Dk.on && !h->ctx->emulated)  // this rank's rows of a partitioned level
+                        b_products_rows(k, t_sp.data(), h->ws_beta(k), Dk.local[0].lo, Dk.local[0].hi);
+                    else
+                        b_products(k, t_sp.data(), h->ws_beta(k));
+                }
             }
         }
         std::vector<CGLevelArgs> a;
         for (int l = 0; l < L; ++l) {
+            if (h->dist[l].on || mf) continue;
             a.push_back(cg_args(h, l, tol, max_iter, h->ws_beta(l), nullptr, alpha_sp[l], ad[l].ptr,
                                 d_it + L * L + l, d_rr + 2 * (L * L + l), d_stat + L * L + l));
             set_coef(a.back(), L * L + l);
         }
-        time_cg(-1);
-        cg_batched(a.data(), L, st, &launches);
-        cg_t.back()->stop();
+        if (!a.empty()) {
+            time_cg(-1);
+            cg_batched(a.data(), (int)a.size(), st, &launches);
+            cg_t.back()->stop();
+        }
+        for (int l = 0; l < L; ++l)
+            if (h->dist[l].on || mf) dist_level(l, tol, true, L, alpha_sp[l], true);
     }
     ttot.stop();
     for (int l = 0; l < L; ++l) ad[l].flush();
@@ -895,11 +1004,20 @@ extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double 
     unsigned long long *d_hits = dalloc<unsigned long long>(1, st);
     MSK_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
     for (int l = 0; l < L; ++l) h->pack(l, h->lev[l].alpha, &launches);
-    if (W > 1) MSK_CUDA(cudaMemsetAsync(sd.ptr, 0, sizeof(double) * (size_t)m, st));
     teval.start();
+    // distributed: rank r evaluates the share [r smax, (r+1) smax) of the sorted
+    // points into a spatial-order buffer; one in-place all-gather of the shares
+    // (not a zero-filled all-reduce) and a permutation give every rank all of
+    // s_L -- or, with MSK_FLAG_OUTPUT_LOCAL, only its own share is written
+    const int64_t smax = (m + W - 1) / W;
+    const bool local_only = (h->flags & MSK_FLAG_OUTPUT_LOCAL) != 0;
+    if (local_only && W > 1 && !h->ctx->emulated && sd.host)  // the other entries keep the caller's values
+        MSK_CUDA(cudaMemcpyAsync(sd.ptr, s, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, st));
+    double *ssp = W > 1 ? dalloc<double>((size_t)(smax * W), st) : nullptr;
     for (int r = 0; r < W; ++r) {
         if (W > 1 && !h->ctx->emulated && r != h->ctx->rank) continue;
-        const int64_t lo = m * r / W, hi = m * (r + 1) / W;
+        const int64_t lo = std::min(m, smax * r), hi = std::min(m, smax * (r + 1));
+        if (hi <= lo) continue;
         GatherArgs ga{};
         ga.d = d;
         ga.k = h->k;
@@ -909,13 +1027,20 @@ extern "C" msk_status msk_evaluate_ex(msk_hierarchy *h, int64_t m, const double 
         for (int l = 0; l < L; ++l) ga.lev[l] = h->view(l, h->lev[l].alpha);
         ga.base = nullptr;
         ga.sign = 1.0;
-        ga.out = sd.ptr;
-        ga.out_perm = perm + lo;
+        ga.out = W > 1 ? ssp + lo : sd.ptr;
+        ga.out_perm = W > 1 ? nullptr : perm + lo;
         ga.hits = d_hits;
         gather(ga, st, &launches);
     }
-    if (W > 1 && !h->ctx->emulated)
-        MSK_NCCL(nccl_api()->AllReduce(sd.ptr, sd.ptr, (size_t)m, ncclFloat64, ncclSum, h->ctx->comm, st));
+    if (W > 1) {
+        const int me = h->ctx->rank;
+        if (!h->ctx->emulated && !local_only)
+            MSK_NCCL(nccl_api()->AllGather(ssp + smax * me, ssp, (size_t)smax, ncclFloat64, h->ctx->comm, st));
+        const bool all = h->ctx->emulated || !local_only;
+        const int64_t lo = all ? 0 : std::min(m, smax * me), hi = all ? m : std::min(m, smax * (me + 1));
+        if (hi > lo) permute_scatter(hi - lo, ssp + lo, perm + lo, sd.ptr, st, &launches);
+        dfree(ssp, st);
+    }
     teval.stop();
     sd.flush();
     ttot.stop();

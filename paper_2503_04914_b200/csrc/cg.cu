@@ -131,15 +131,31 @@ __device__ __forceinline__ void group_barrier(unsigned long long *ctr, int nb,
     }
 }
 
+// Per-thread share of a fixed-order chunk sum: partials j = tid, tid + NT, ...
+// added left to right (the order every reduction of the solver uses).  The
+// loads are issued 8 at a time ahead of the dependent adds (one L2 round trip
+// per 8 partials instead of per partial); the summation order is unchanged.
+__device__ __forceinline__ double strided_sum(const double *partials, int64_t nchunks) {
+    double t = 0.0;
+    int64_t j = threadIdx.x;
+    for (; j + 7 * NT < nchunks; j += 8 * NT) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(&partials[j + u * NT]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t += v[u];
+    }
+    for (; j < nchunks; j += NT) t += __ldcg(&partials[j]);
+    return t;
+}
+
 // Deterministic all-reduce over the chunk partials of one group: after the
 // group barrier every CTA sums all partials in the same fixed order.
 __device__ __forceinline__ double chunk_allreduce(const double *partials, int64_t nchunks, int nb,
                                                   unsigned long long *ctr,
                                                   unsigned long long &round, double *s_red) {
     group_barrier(ctr, nb, round);
-    double t = 0.0;
-    for (int64_t j = threadIdx.x; j < nchunks; j += NT) t += __ldcg(&partials[j]);
-    return block_sum<NT>(t, s_red);
+    return block_sum<NT>(strided_sum(partials, nchunks), s_red);
 }
 
 // ---------------------------------------------------------------------------
@@ -526,7 +542,19 @@ __device__ __forceinline__ void chunk_allreduce_r(const double *partials, int64_
     group_barrier(ctr, nb, round);
 #pragma unroll
     for (int r = 0; r < R; ++r) out[r] = 0.0;
-    for (int64_t j = threadIdx.x; j < nchunks; j += NT) {
+    int64_t j = threadIdx.x;
+    for (; j + 3 * NT < nchunks; j += 4 * NT) {  // loads ahead of the adds, same order (strided_sum)
+        double v[4][R];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[u][r] = __ldcg(&partials[(j + u * NT) * R + r]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < R; ++r) out[r] += v[u][r];
+    }
+    for (; j < nchunks; j += NT) {
 #pragma unroll
         for (int r = 0; r < R; ++r) out[r] += __ldcg(&partials[j * R + r]);
     }
@@ -885,8 +913,14 @@ __device__ __forceinline__ void dcg_check_top(DistCGScalars &s, double tol2, int
 // Partitioned CG over peer memory (PeerCGArgs, kernels.cuh).  One persistent
 // cooperative launch per rank runs the whole CG of its row block; W ranks in
 // ONE launch in the single-GPU emulation (rank = blockIdx.x / nb).
-__device__ __forceinline__ void red_release_sys_add(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_sys_add(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
@@ -897,9 +931,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // the fixed-order chunk sum of chunk_allreduce (no barrier: the caller's
 // cross-rank barrier has made every chunk partial visible)
 __device__ __forceinline__ double chunk_sum(const double *partials, int64_t nchunks, double *s_red) {
-    double t = 0.0;
-    for (int64_t j = threadIdx.x; j < nchunks; j += NT) t += __ldcg(&partials[j]);
-    return block_sum<NT>(t, s_red);
+    return block_sum<NT>(strided_sum(partials, nchunks), s_red);
 }
 
 struct PeerPush {  // thread 0 stores a chunk partial into every rank's copy
@@ -940,23 +972,32 @@ __global__ void __launch_bounds__(NT, MB) k_pcg(const __grid_constant__ PeerCGAr
     // the rank's CTAs meet (group barrier), its leader adds 1 to every rank's
     // counter (release, system scope), every CTA waits for W arrivals (acquire)
     auto xbarrier = [&]() {
-        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) fence_acq_rel_sys();  // cumulative: the CTA's peer stores, ordered by the bar.sync
         group_barrier(Rm.gbar, nb, round);
         ++xround;
-        if (me == 0 && tid == 0)
-            for (int w = 0; w < W; ++w) red_release_sys_add(A.R[w].xcnt, 1ull);
+        if (me == 0 && tid == 0) {
+            // one system-scope release fence, then relaxed adds (fence + relaxed
+            // write = release); the group barrier's acquire made every CTA's
+            // stores (each fenced above) happen-before this fence
+            fence_acq_rel_sys();
+            for (int w = 0; w < W; ++w) red_relaxed_sys_add(A.R[w].xcnt, 1ull);
+        }
         if (tid == 0) {
             const unsigned long long want = (unsigned long long)W * xround;
             unsigned long long spins = 0;
-            while (ld_acquire_sys(Rm.xcnt) < want) {
-                __nanosleep(64);
+            while (ld_relaxed_sys(Rm.xcnt) < want) {  // poll relaxed, then one acquire
+                __nanosleep(32);
                 if (++spins > (1ull << 31)) __trap();  // never hang the device forever
             }
+            (void)ld_acquire_sys(Rm.xcnt);
         }
         __syncthreads();
     };
     // r of a row this rank owns -> the peers whose SpMV reads it (their halo)
+    const int64_t slo = Rm.slo, shi = Rm.shi;
     auto push_halo = [&](int64_t i, double v) {
+        if (i < slo || i >= shi) return;  // interior row: no peer reads it
         for (int w = 0; w < W; ++w)
             if (w != m && i >= A.R[w].hlo && i < A.R[w].hhi) A.R[w].r[i] = v;
     };
@@ -1290,7 +1331,15 @@ __global__ void __launch_bounds__(NT) k_dcg_scalar(DistCGArgs A, int mode) {
     double v = 0.0;
     if (mode != 3) {
         double t = 0.0;
-        for (int64_t j = threadIdx.x; j < A.nchunks; j += NT) t += A.part_recv[j];
+        if (A.gw == 0) {
+            t = strided_sum(A.part_recv, A.nchunks);
+        } else {  // all-gathered blocks: the same chunks in the same order
+            int r = 0;
+            for (int64_t j = threadIdx.x; j < A.nchunks; j += NT) {
+                while (j >= A.gc0[r + 1]) ++r;
+                t += __ldcg(&A.part_recv[r * A.gcmax + j - A.gc0[r]]);
+            }
+        }
         v = block_sum<NT>(t, red);
     }
     if (threadIdx.x != 0) return;

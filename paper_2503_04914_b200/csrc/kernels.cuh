@@ -171,9 +171,13 @@ struct DistCGArgs {
     CGLevelArgs L;             // n, tol2, max_iter, chunk_tiles, vectors (full length, owned rows
                                // valid), row_ptr indexed by GLOBAL row (local storage - lo), col/val local
     int64_t c0, c1, nchunks;   // owned chunks [c0, c1) of nchunks
-    double *part_send;         // nchunks, zero outside the owned chunks
-    const double *part_recv;   // nchunks after the all-reduce
+    double *part_send;         // indexed by chunk (the owned chunks are written)
+    const double *part_recv;   // gw == 0: nchunks partials by chunk; gw > 0: the all-gathered
+                               // blocks, chunk c of rank r at r * gcmax + c - gc0[r]
     DistCGScalars *sc;
+    int gw;
+    int64_t gcmax;
+    int64_t gc0[kMaxParts + 1];
 };
 struct DistPtrs {
     const double *p[kMaxParts];
@@ -218,6 +222,7 @@ struct PeerRank {
     const double *val;
     int64_t c0, c1;             // owned chunks [c0, c1)
     int64_t hlo, hhi;           // rows this rank's SpMV reads (owned rows and halo)
+    int64_t slo, shi;           // owned rows some peer reads (the union of the send ranges)
 };
 struct PeerCGArgs {
     CGLevelArgs L;              // n, nnz, b / b_src / b_perm, tol2, max_iter, chunk_tiles, out_*, coef

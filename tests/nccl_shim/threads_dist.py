@@ -39,20 +39,27 @@ CASES = [  # (name, hierarchy, T, patch_R, flags of the rank contexts' hierarchi
     ("halton3d-T3-patch", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 3.0, 9.0, DIST_ALL),
     # bench.py's setting (no DIST_ALL): only the 1.25M-point level (>= 2^20) is partitioned
     ("C3P5-default", lambda: config("C3P5", m_eval=0), 0.0, 0.0, 0),
+    # the LITERAL schedule (Algorithm 2 as printed) with partitioned levels
+    ("halton3d-literal", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 0.0, 0.0, DIST_ALL),
+    ("C3P4-literal", lambda: config("C3P4", m_eval=0), 0.0, 0.0, DIST_ALL),
+    # MSK_FLAG_OUTPUT_LOCAL: each rank writes only its share of s_L (no all-gather)
+    ("C3P4-local", lambda: config("C3P4", m_eval=0), 0.0, 0.0, DIST_ALL | msk.MSK_FLAG_OUTPUT_LOCAL),
 ]
 FULL = [("C3-default", lambda: config("C3", m_eval=0), 0.0, 0.0, 0)]
 
 
-def run(ctx, H, f, x, T, patch_R, flags):
+def run(ctx, H, f, x, T, patch_R, flags, schedule="pruned"):
     h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=flags)
     h.assemble(T=T, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=1000)
-    a, info = h.solve(f, tol=1e-12)
+    a, info = h.solve(f, tol=1e-12, schedule=schedule)
     out = {"alpha": a, "iters": list(info.cg_iters)[:H.L]}
     if T > 0:
         h.set_threshold(1.0)
         out["alpha_T1"], _ = h.solve(f, tol=1e-12)
     else:
-        out["s"], _ = h.evaluate(x)
+        s = np.full(x.shape[0], np.nan)
+        h.evaluate(x, out=s)
+        out["s"] = s
     h.close()
     return out
 
@@ -70,7 +77,8 @@ def main(world: int, full: bool = False) -> None:
         f = H.f()
         x = uniform_points(10 ** 6 if full else 5000, H.d, seed=4)
         c1 = msk.Context(0)
-        ref = run(c1, H, f, x, T, patch_R, 0)  # also initialises libmsk's per-process state
+        sched = "literal" if name.endswith("-literal") else "pruned"
+        ref = run(c1, H, f, x, T, patch_R, 0, sched)  # also initialises libmsk's per-process state
         c1.close()
         nid = msk.msk_nccl_unique_id()
         res, err = [None] * world, [None] * world
@@ -78,7 +86,7 @@ def main(world: int, full: bool = False) -> None:
         def rank_main(r):
             try:
                 ctx = msk.Context(0, None, r, world, nid)
-                res[r] = run(ctx, H, f, x, T, patch_R, flags)
+                res[r] = run(ctx, H, f, x, T, patch_R, flags, sched)
                 ctx.close()
             except BaseException as e:  # reported by the main thread
                 err[r] = e
@@ -101,8 +109,14 @@ def main(world: int, full: bool = False) -> None:
             if T > 0:
                 for l in range(H.L):
                     assert np.array_equal(got["alpha_T1"][l], ref["alpha_T1"][l]), (name, r, l, "T=1")
+            elif flags & msk.MSK_FLAG_OUTPUT_LOCAL:
+                w = ~np.isnan(got["s"])  # this rank's share only, each value exact
+                assert w.any() and np.array_equal(got["s"][w], ref["s"][w]), (name, r, "s_L share")
             else:
                 assert np.array_equal(got["s"], ref["s"]), (name, r, "s_L")
+        if flags & msk.MSK_FLAG_OUTPUT_LOCAL:  # the shares partition the points
+            cover = sum((~np.isnan(res[r]["s"])).astype(int) for r in range(world))
+            assert np.all(cover == 1), (name, "shares")
         # the transport really carried the solve: per-rank init, halos, reductions
         assert s1["comm_init"] == world and s1["allgather"] > 0 and s1["allreduce"] > 0, s1
         assert s1["send"] > 0 and s1["send"] == s1["recv"], s1

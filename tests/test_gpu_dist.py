@@ -67,9 +67,9 @@ def test_partitioned_equals_single_gpu_bitwise(msk, name, world, path, monkeypat
 
 
 def test_partitioned_matches_oracle_and_default_threshold(msk):
-    """C3 4-level prefix: with the default threshold (>= 2^20 points) no level
-    is partitioned; with DIST_ALL every level with >= world chunks is.  Both
-    match the oracle within the 1e-9 bar."""
+    """C3 4-level prefix: with the default threshold no level is partitioned;
+    with DIST_ALL every level with >= world chunks is.  Both match the oracle
+    within the 1e-9 bar."""
     H = config("C3P4", m_eval=0)
     f = H.f()
     cw = msk.Context(0, rank=-1, world=4)
@@ -80,9 +80,6 @@ def test_partitioned_matches_oracle_and_default_threshold(msk):
         ao, _, _ = oracle.sequential(H.points, H.delta, f, tol=1e-12, direct_max_n=0)
         for l in range(H.L):
             assert np.linalg.norm(a[l] - ao[l]) <= 1e-9 * np.linalg.norm(ao[l])
-    with pytest.raises(msk.MskError) as ei:
-        h.solve(f, schedule="literal")
-    assert ei.value.status == 1
     with pytest.raises(msk.MskError) as ei:
         h.cg_level(3, f[3])
     assert ei.value.status == 6
@@ -121,3 +118,28 @@ def test_partitioned_thresholded_equals_single_gpu_bitwise(msk, name, T, patch_R
     assert list(nAw) == list(nA)
     for x, y in zip(fac, facw):
         assert all(np.array_equal(u, v) for u, v in zip(x[:3], y[:3]))
+
+
+@pytest.mark.parametrize("name", ["halton3d", "C3P4"])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("path", ["p2p", "phase"])
+def test_partitioned_literal_schedule_bitwise(msk, name, world, path, monkeypatch):
+    """The LITERAL schedule (Algorithm 2 as printed: L sweeps of
+    inner solves on levels 1..L-1 + B products, then the block CG) with
+    partitioned levels: every inner and final solve of a partitioned level is
+    the partitioned CG; bit-identical to the single-GPU literal solve."""
+    monkeypatch.setenv("MSK_DIST_P2P", "1" if path == "p2p" else "0")
+    H = HIERS[name]()
+    f = H.f()
+    out = []
+    for ctx, flags in ((msk.Context(0), 0), (msk.Context(0, rank=-1, world=world), msk.MSK_FLAG_DIST_ALL)):
+        h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k, flags=flags)
+        h.assemble()
+        a, info = h.solve(f, tol=1e-12, schedule="literal")
+        out.append((a, list(info.cg_iters)[:H.L], list(info.inner_iters)[:H.L], info.jacobi_sweeps))
+        h.close()
+        ctx.close()
+    (a1, i1, n1, s1), (aw, iw, nw, sw) = out
+    assert sw == s1 == H.L and iw == i1 and nw == n1
+    for l in range(H.L):
+        assert np.array_equal(aw[l], a1[l]), (name, world, l)
