@@ -551,8 +551,8 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
     }
     for (int l = 0; l < h->L; ++l) {
         LevelData &D = h->lev[l];
-        dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st);
-        D.row_ptr = nullptr; D.col = nullptr; D.val = nullptr;
+        dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st); dfree(D.col16, st); dfree(D.cbase, st);
+        D.row_ptr = nullptr; D.col = nullptr; D.val = nullptr; D.col16 = nullptr; D.cbase = nullptr;
         nnz[l] = 0;
         D.nnz = 0;  // (partitioned levels accumulate their partitions' entries below)
         if (h->dist[l].on) {  // owned rows only, per local partition
@@ -649,6 +649,20 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
         MSK_CUDA(cudaMemsetAsync(D.val + D.nnz, 0, 2 * sizeof(double), st));
         LevelView v = h->view(l);
         fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
+        // k_cg's 10 B/nnz stream: 16-bit columns in per-chunk windows (MSK_COL16=0: off)
+        static const bool c16 = !(getenv("MSK_COL16") && getenv("MSK_COL16")[0] == '0');
+        if (c16 && D.n >= 256) {
+            const int CH = cg_chunk_tiles(D.n);
+            const int64_t nch = ((D.n + 255) / 256 + CH - 1) / CH;
+            D.col16 = dalloc<uint16_t>((size_t)D.nnz + 16, st);
+            D.cbase = dalloc<int4>((size_t)nch, st);
+            MSK_CUDA(cudaMemsetAsync(D.col16 + D.nnz, 0, 16 * sizeof(uint16_t), st));
+            launches += 1;
+            if (!col16_build(D.n, D.row_ptr, D.col, D.col16, D.cbase, st)) {
+                dfree(D.col16, st); dfree(D.cbase, st);
+                D.col16 = nullptr; D.cbase = nullptr;
+            }
+        }
     }
     if (T > 0.0 && h->L > 1) build_factor(h, T, lagrange_tol, patch_R, patch_min_n, &launches);
     tm.stop();

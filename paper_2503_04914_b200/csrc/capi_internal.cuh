@@ -58,6 +58,8 @@ struct LevelData {
     int64_t *row_ptr = nullptr;
     int32_t *col = nullptr;
     double *val = nullptr;
+    uint16_t *col16 = nullptr;     // 16-bit columns for k_cg (cg.cu col16_build), or null
+    int4 *cbase = nullptr;         //   their window bases per reduction chunk
     double *alpha = nullptr;       // coefficients of the last solve, spatial order
     double4 *rec = nullptr;        // packed (coords, coefficient) records for gathers
     float4 *frec = nullptr;        // FP32 coordinates relative to lo (gather prefilter)
@@ -368,6 +370,7 @@ struct msk_hierarchy {
             LevelData &D = lev[l];
             dfree(D.xs, s); dfree(D.perm, s); dfree(D.cell_start, s); dfree(D.cnt, s);
             dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s); dfree(D.rec, s); dfree(D.frec, s);
+            dfree(D.col16, s); dfree(D.cbase, s);
             D = LevelData();
         }
         dfree(ws, s);

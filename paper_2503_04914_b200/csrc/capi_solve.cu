@@ -21,6 +21,8 @@ CGLevelArgs cg_args(msk_hierarchy *h, int l, double tol, int max_iter, const dou
     a.row_ptr = D.row_ptr;
     a.col = D.col;
     a.val = D.val;
+    a.col16 = D.col16;
+    a.cbase = D.cbase;
     a.b = b;
     a.b_src = b_src;
     a.b_perm = b_src ? D.perm : nullptr;
@@ -406,6 +408,8 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             A.L.row_ptr = P.rp ? P.rp - P.lo : nullptr;  // indexed by global row
             A.L.col = P.col;
             A.L.val = P.val;
+            A.L.col16 = nullptr;
+            A.L.cbase = nullptr;
             A.L.nnz = P.nnz;
             A.L.chunk_tiles = CH;
             A.c0 = P.c0;

@@ -194,6 +194,25 @@ __device__ __forceinline__ void issue_piece_t(SH &S, int b, const int32_t *col, 
     tma_load_1d(S.st[b].col, col + clo, cb, &S.bar_st[b], pol);
 }
 
+// the same piece with 16-bit columns (col16): the stage's column area holds 2 x
+// (C + 8) of them
+template <class SH>
+__device__ __forceinline__ void issue_piece_16(SH &S, int b, const uint16_t *col16, const double *val,
+                                               int64_t kb, int64_t ke, uint64_t pol) {
+    const int64_t vlo = kb & ~(int64_t)1, vhi = (ke + 1) & ~(int64_t)1;
+    const int64_t clo = kb & ~(int64_t)7, chi = (ke + 7) & ~(int64_t)7;
+    const uint32_t vb = (uint32_t)((vhi - vlo) * 8), cb = (uint32_t)((chi - clo) * 2);
+    mbar_arrive_expect_tx(&S.bar_st[b], vb + cb);
+    tma_load_1d(S.st[b].val, val + vlo, vb, &S.bar_st[b], pol);
+    tma_load_1d(S.st[b].col, col16 + clo, cb, &S.bar_st[b], pol);
+}
+
+__device__ __forceinline__ int col16_decode(uint32_t c, const int4 &b) {
+    const uint32_t w = c >> 14;
+    const int base = w == 0 ? b.x : w == 1 ? b.y : w == 2 ? b.z : b.w;
+    return base + (int)(c & 0x3FFFu);
+}
+
 // Chunks handled: cbase + me + k*nb for k = 0.. while < cbase + nloc (cbase =
 // 0, nloc = all chunks on one GPU; the owned chunk range of a partition in
 // the distributed CG).  L.row_ptr is indexed by global row.
@@ -201,11 +220,16 @@ __device__ __forceinline__ void issue_piece_t(SH &S, int b, const int32_t *col, 
 struct NoPush {
     __device__ __forceinline__ void operator()(int64_t, double) const {}
 };
-template <int C, bool PLAIN = false, class Push = NoPush>
+template <int C, bool PLAIN = false, class Push = NoPush, bool C16 = false>
 __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
                                            int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol,
                                            bool first, double alpha_prev, double beta,
                                            const Push &push = Push()) {
+    // C16: 16-bit columns (L.col16 + per-chunk window bases L.cbase), 10 B per entry
+    auto issue = [&](int b, int64_t kb, int64_t ke) {
+        if constexpr (C16) issue_piece_16(S, b, L.col16, L.val, kb, ke, pol);
+        else issue_piece_t(S, b, L.col, L.val, kb, ke, pol);
+    };
     constexpr int CAPTE = C - 2;  // usable entries per piece (alignment slack)
     // Asynchronous stage release (pieces of >= MSK_ASYNC_MIN_C entries): when
     // piece j + 2 lies in the same chunk, the last warp to finish piece j
@@ -240,7 +264,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
     {
         const int64_t *rp = S.rp[ps.CS & 1] + rp_off(cr0);
         const int64_t K0 = rp[0], K1 = rp[crows];
-        if (tid == 0) issue_piece_t(S, ps.P & 1, L.col, L.val, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1, pol);
+        if (tid == 0) issue(ps.P & 1, K0, K0 + CAPTE < K1 ? K0 + CAPTE : K1);
     }
     for (int64_t k = 0; k < K; ++k) {
         chunk_rows(k, cr0, crows);
@@ -260,6 +284,8 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
         }
         const int64_t *rp = S.rp[cs & 1] + rp_off(cr0);
         const int64_t K1 = rp[crows];
+        int4 wb = make_int4(0, 0, 0, 0);
+        if constexpr (C16) wb = __ldg(&L.cbase[cbase + me + k * nb]);
         int64_t rb[MAXCH], re[MAXCH];
         double acc[MAXCH];
 #pragma unroll
@@ -279,7 +305,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             const bool pre_issued = ASYNC && kb != rp[0];
             if (ke < K1) {
                 if (tid == 0 && !pre_issued)
-                    issue_piece_t(S, (ps.P + 1) & 1, L.col, L.val, ke, ke + CAPTE < K1 ? ke + CAPTE : K1, pol);
+                    issue((ps.P + 1) & 1, ke, ke + CAPTE < K1 ? ke + CAPTE : K1);
             } else if (k + 1 < K) {
                 mbar_wait(&S.bar_rp[(cs + 1) & 1], ((cs + 1) >> 1) & 1u);
                 if (tid == 0) {
@@ -288,12 +314,13 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
                     chunk_rows(k + 1, nr0, nrows);
                     const int64_t *nrp = S.rp[(cs + 1) & 1] + rp_off(nr0);
                     const int64_t a = nrp[0], e = nrp[nrows];
-                    issue_piece_t(S, (ps.P + 1) & 1, L.col, L.val, a, a + CAPTE < e ? a + CAPTE : e, pol);
+                    issue((ps.P + 1) & 1, a, a + CAPTE < e ? a + CAPTE : e);
                 }
             }
             mbar_wait(&S.bar_st[ps.P & 1], (ps.P >> 1) & 1u);
             const CtaStageT<C> &cur = S.st[ps.P & 1];
-            const int voff = (int)(kb & 1), coff = (int)(kb & 3);
+            const int voff = (int)(kb & 1), coff = C16 ? (int)(kb & 7) : (int)(kb & 3);
+            const uint16_t *col16 = reinterpret_cast<const uint16_t *>(cur.col);
 #pragma unroll
             for (int t = 0; t < MAXCH; ++t) {
                 if (t >= CH) break;
@@ -306,9 +333,10 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int ee = e + u;
-                        MSK_DASSERT(ee >= hi || (coff + ee < C + 8 && voff + ee < C && cur.col[coff + ee] >= 0 &&
-                                                 cur.col[coff + ee] < n));
-                        pv[u] = ee < hi ? rv[cur.col[coff + ee]] : 0.0;
+                        const int cj = ee < hi ? (C16 ? col16_decode(col16[coff + ee], wb) : cur.col[coff + ee]) : 0;
+                        MSK_DASSERT(ee >= hi || (coff + ee < (C16 ? 2 * (C + 8) : C + 8) && voff + ee < C &&
+                                                 cj >= 0 && cj < n));
+                        pv[u] = ee < hi ? rv[cj] : 0.0;
                         vv[u] = ee < hi ? cur.val[voff + ee] : 0.0;
                     }
 #pragma unroll
@@ -334,7 +362,7 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
                     if (old % NW == NW - 1) {
                         fence_proxy_async_smem();
                         const int64_t k2 = kb + 2 * CAPTE;
-                        issue_piece_t(S, ps.P & 1, L.col, L.val, k2, k2 + CAPTE < K1 ? k2 + CAPTE : K1, pol);
+                        issue(ps.P & 1, k2, k2 + CAPTE < K1 ? k2 + CAPTE : K1);
                     }
                 }
             } else {
@@ -459,7 +487,11 @@ __global__ void __launch_bounds__(NT, MB) k_cg(CGBatch B) {
             if (it >= L.max_iter) { status = 1; break; }
             tick(-1);
             // ---- w = A r ; p = r + beta p ; q = w + beta q ; x += alpha p_old ; pq = p.q
-            spmv_phase(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol, it == 0, alpha, beta);
+            if (L.col16)
+                spmv_phase<C, false, NoPush, true>(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol, it == 0,
+                                                   alpha, beta);
+            else
+                spmv_phase(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol, it == 0, alpha, beta);
             tick(0);
             const double pq = chunk_allreduce(part + nchunks, nchunks, nb, L.barrier, round, S.red);
             tick(1);
@@ -1632,6 +1664,52 @@ unsigned dcg_grid(const DistCGArgs &a, int per_sm) {
 }
 }  // namespace
 
+// 16-bit columns per reduction chunk: greedy windows of 2^14 indices from the
+// smallest column up (at most 4; a chunk's columns fall into ~3 clusters, one
+// per x-offset of its rows' cells), entry = window << 14 | (column - base).
+__global__ void __launch_bounds__(NT) k_col16(int64_t n, int CH, const int64_t *__restrict__ rp,
+                                              const int32_t *__restrict__ col, uint16_t *__restrict__ col16,
+                                              int4 *__restrict__ cbase, int *__restrict__ fail) {
+    __shared__ int red[NW];
+    const int64_t c = blockIdx.x;
+    const int64_t r0 = c * CH * NT, r1 = r0 + (int64_t)CH * NT < n ? r0 + (int64_t)CH * NT : n;
+    const int64_t e0 = rp[r0], e1 = rp[r1];
+    const int tid = threadIdx.x;
+    auto block_min = [&](int v) {
+        v = __reduce_min_sync(0xffffffffu, v);
+        __syncthreads();
+        if ((tid & 31) == 0) red[tid >> 5] = v;
+        __syncthreads();
+        int m = red[0];
+        for (int w = 1; w < NW; ++w) m = red[w] < m ? red[w] : m;
+        return m;
+    };
+    int base[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+    int64_t lower = INT64_MIN;
+    for (int w = 0; w < 4; ++w) {
+        int m = INT_MAX;
+        for (int64_t e = e0 + tid; e < e1; e += NT) {
+            const int v = col[e];
+            if ((int64_t)v >= lower && v < m) m = v;
+        }
+        m = block_min(m);
+        if (m == INT_MAX) break;
+        base[w] = m;
+        lower = (int64_t)m + 16384;
+    }
+    for (int64_t e = e0 + tid; e < e1; e += NT) {
+        const int v = col[e];
+        const int w = (v >= base[1]) + (v >= base[2]) + (v >= base[3]);
+        const int64_t off = (int64_t)v - base[w];
+        if (off < 0 || off >= 16384) {
+            atomicOr(fail, 1);
+            continue;
+        }
+        col16[e] = (uint16_t)((w << 14) | (int)off);
+    }
+    if (tid == 0) cbase[c] = make_int4(base[0], base[1], base[2], base[3]);
+}
+
 // co-resident CTAs of k_pcg's variant for a level (the per-rank grid is
 // this / W in the emulation, all of it on a GPU of its own)
 int pcg_resident_blocks(double nnz, double rows) {
@@ -1649,6 +1727,22 @@ void pcg_launch(const PeerCGArgs &a, cudaStream_t st) {
     PeerCGArgs A = a;
     void *args[] = {&A};
     MSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NT), args, var.smem, st));
+}
+
+bool col16_build(int64_t n, const int64_t *row_ptr, const int32_t *col, uint16_t *col16, int4 *cbase,
+                 cudaStream_t st) {
+    if (n <= 0) return false;
+    const int CH = cg_chunk_tiles(n);
+    const int64_t nch = ((n + NT - 1) / NT + CH - 1) / CH;
+    int *fail = nullptr, hf = 0;
+    MSK_CUDA(cudaMallocAsync((void **)&fail, sizeof(int), st));
+    MSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), st));
+    k_col16<<<(unsigned)nch, NT, 0, st>>>(n, CH, row_ptr, col, col16, cbase, fail);
+    MSK_CHECK_LAUNCH();
+    MSK_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    MSK_CUDA(cudaFreeAsync(fail, st));
+    return hf == 0;
 }
 
 void dcg_init(const DistCGArgs &a, cudaStream_t st) {

@@ -133,6 +133,10 @@ struct CGLevelArgs {
     unsigned long long *dbg;  // optional: 6 phase times (ns) of CTA 0 (spmv, bar1, r, bar2, -, -)
     double *coef;             // optional: CG scalars (alpha_k, beta_k) of iterations k < coef_cap
     int coef_cap;             //   (Lanczos tridiagonal -> kappa estimate, msk_solve_info.kappa_est)
+    // optional 16-bit columns (cg.cu col16_build): entry -> (window << 14 | offset), the
+    // column = cbase[chunk].{x,y,z,w}[window] + offset; k_cg streams these instead of col
+    const uint16_t *col16;
+    const int4 *cbase;        // per reduction chunk (chunk_tiles * 256 rows): 4 window bases
 };
 // ---- multi-RHS CG (msk_solve_multi; cg.cu): one level, R right-hand sides
 // with their own scalars; per column the arithmetic of k_cg (bit-identical to
@@ -201,6 +205,11 @@ void col_minmax(int64_t nnz, const int32_t *col, unsigned long long *mm, cudaStr
 // CSR arrays must be 16-byte aligned and padded: row_ptr n+3 entries,
 // col nnz+4, val nnz+2 (bulk copies round their extents to 16 bytes).
 int cg_max_resident_blocks();
+// 16-bit column encoding of a level's CSR per reduction chunk (k_cg's 10 B/nnz
+// stream): returns false (and writes nothing usable) when some chunk's columns
+// need more than 4 windows of 2^14 indices
+bool col16_build(int64_t n, const int64_t *row_ptr, const int32_t *col, uint16_t *col16, int4 *cbase,
+                 cudaStream_t st);
 
 // ---- partitioned CG over peer memory (cg.cu k_pcg): the
 // whole CG of a row-partitioned level in ONE persistent launch per rank.
