@@ -207,10 +207,12 @@ __device__ __forceinline__ void issue_piece_16(SH &S, int b, const uint16_t *col
     tma_load_1d(S.st[b].col, col16 + clo, cb, &S.bar_st[b], pol);
 }
 
+// branch-free (lanes of a warp use different windows): two-way selects only
 __device__ __forceinline__ int col16_decode(uint32_t c, const int4 &b) {
-    const uint32_t w = c >> 14;
-    const int base = w == 0 ? b.x : w == 1 ? b.y : w == 2 ? b.z : b.w;
-    return base + (int)(c & 0x3FFFu);
+    const bool odd = (c >> 14) & 1u, upper = (c >> 15) & 1u;
+    const int lo = odd ? b.y : b.x;
+    const int hi = odd ? b.w : b.z;
+    return (upper ? hi : lo) + (int)(c & 0x3FFFu);
 }
 
 // Chunks handled: cbase + me + k*nb for k = 0.. while < cbase + nloc (cbase =

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--schedule", default="pruned")
     ap.add_argument("--tol", type=float, default=1e-12)
     ap.add_argument("--m-eval", type=int, default=100_000)
+    ap.add_argument("--matrix-free", action="store_true",
+                    help="MSK_FLAG_MATRIX_FREE (the paper's mode: no stored matrices, P:1559)")
     args = ap.parse_args()
     import torch
     import paper_2503_04914_b200 as msk
@@ -37,7 +39,8 @@ def main():
     ctx = msk.Context(0, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     t1 = time.time()
-    h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=1)
+    h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=1,
+                      flags=msk.MSK_FLAG_MATRIX_FREE if args.matrix_free else 0)
     h.assemble()
     alpha, si = h.solve(f, tol=args.tol, schedule=args.schedule)
     s, ei = h.evaluate(xe)
@@ -50,6 +53,7 @@ def main():
     err = float((sL - f[-1][idx]).abs().max() / f[-1].abs().max())
     L = H.L
     out = {"levels": L, "points": int(sum(H.n)), "schedule": args.schedule, "tol": args.tol,
+           "matrix_free": bool(args.matrix_free),
            "wall_s": wall, "gen_s": t_gen,
            "t_create_ms": hi.t_create_ms, "t_assemble_ms": hi.t_assemble_ms,
            "t_solve_ms": si.t_total_ms, "t_cg_ms": si.t_cg_ms, "t_b_ms": si.t_gather_ms,
