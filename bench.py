@@ -15,7 +15,7 @@ evaluation), DESIGN.md §Measurement.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl msk|reference]
 
 N > 1 (torchrun): one rank per GPU solves the SAME problem partitioned across
-the ranks (levels with >= 2^20 points split into spatially sorted row blocks,
+the ranks (large levels -- a latency model decides, DESIGN.md §10 -- split into spatially sorted row blocks,
 p halos exchanged and CG chunk partials all-reduced over NCCL; smaller levels
 solved redundantly) -- strong scaling, DESIGN.md §Multi-GPU.  value = the
 problem's Wendland nonzeros per step (identical for every N: the partitioned

@@ -69,8 +69,11 @@ typedef enum {
 /* msk_hierarchy_create flags */
 #define MSK_FLAG_NONE 0u
 #define MSK_FLAG_DIST_ALL 1u /* distributed context: partition every level that has at least world
-                                row chunks (default: only levels with >= 2^20 points; smaller
-                                levels are solved redundantly on every rank) */
+                                row chunks (default: the levels whose CG iteration a latency model
+                                says gets faster split over the ranks -- bytes per iteration vs a
+                                ~15 us floor plus the partitioned path's barriers, DESIGN.md §10;
+                                on C3 the 1.25M- and 1e7-point levels; the others are solved
+                                redundantly on every rank) */
 #define MSK_FLAG_MATRIX_FREE 2u /* a3 matrix-free: A_l is never stored;
                                    every CG SpMV evaluates Phi on the fly over the level's cell list,
                                    visiting the columns in the stored CSR order, so alpha is

@@ -488,6 +488,23 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
 
 namespace {
 void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch_R, int64_t patch_min_n, bool mf);
+
+// Which levels to partition: a latency model of one CG
+// iteration.  One GPU moves ~12 nnz + 88 n bytes at ~5 TB/s (measured k_cg:
+// 4.9-5.4 TB/s), with a ~15 us floor (two device barriers and the grid's
+// ramp; C3 levels 1-4 measure 5-15 us); W partitions move 1/W of the bytes
+// each and add the partitioned path's barriers (k_pcg over NVLink: ~10 us
+// per iteration; host-driven phase path with NCCL: ~60 us).  Partition when
+// that is below 0.8 x the one-GPU time.  Identical on every rank (same inputs).
+bool partition_pays(double nnz, double n, int W) {
+    const char *e = getenv("MSK_DIST_P2P");
+    const bool p2p = !(e && e[0] == '0');
+    const double bw = 5e12, floor_s = 15e-6, ovh = p2p ? 10e-6 : 60e-6;
+    const double bytes = 12.0 * nnz + 88.0 * n;
+    const double t1 = std::max(floor_s, bytes / bw);
+    const double tw = std::max(floor_s, bytes / ((double)W * bw)) + ovh;
+    return tw < 0.8 * t1;
+}
 }
 
 extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrange_tol, double patch_R,
@@ -532,7 +549,8 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
         const int64_t n = h->lev[l].n;
         const int64_t rpc = (int64_t)cg_chunk_tiles(n) * 256;
         const int64_t nch = (n + rpc - 1) / rpc;
-        if (nch >= W && ((h->flags & MSK_FLAG_DIST_ALL) || n >= (1ll << 20))) {
+        if (nch >= W && ((h->flags & MSK_FLAG_DIST_ALL) ||
+                         partition_pays((double)sum_i32(h->lev[l].cnt, n, st), (double)n, W))) {
             auto &Dd = h->dist[l];
             Dd.on = true;
             Dd.rows.resize(W + 1);
@@ -649,8 +667,11 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
         MSK_CUDA(cudaMemsetAsync(D.val + D.nnz, 0, 2 * sizeof(double), st));
         LevelView v = h->view(l);
         fill_pattern(h->d, h->k, v, v, D.row_ptr, D.col, D.val, st, &launches);
-        // k_cg's 10 B/nnz stream: 16-bit columns in per-chunk windows (MSK_COL16=0: off)
-        static const bool c16 = !(getenv("MSK_COL16") && getenv("MSK_COL16")[0] == '0');
+        // MSK_COL16=1: k_cg streams 16-bit columns in per-chunk windows (10 B/nnz instead
+        // of 12).  Off by default: same-box A/B C3 finest level 40.1 vs
+        // 32.7 ms, C2 21.3 vs 19.4 ms -- the decode lengthens the gather's address chain,
+        // and the SpMV pass is gather-latency bound, not bandwidth bound
+        static const bool c16 = getenv("MSK_COL16") && getenv("MSK_COL16")[0] == '1';
         if (c16 && D.n >= 256) {
             const int CH = cg_chunk_tiles(D.n);
             const int64_t nch = ((D.n + 255) / 256 + CH - 1) / CH;

@@ -352,6 +352,7 @@ int64_t bucket_count(const uint8_t *bucket, int64_t nnz, int tmax, cudaStream_t 
 void minmax_points(int64_t n, int d, const double *pts, unsigned long long *mm, cudaStream_t st,
                    int *launches);
 double ord_key_to_double(unsigned long long k);
+int64_t sum_i32(const int32_t *v, int64_t n, cudaStream_t st);
 void permute_gather(int64_t n, const double *src, const int32_t *perm, double *dst,
                     cudaStream_t st, int *launches);  // dst[i] = src[perm[i]]
 void permute_scatter(int64_t n, const double *src, const int32_t *perm, double *dst,

@@ -54,7 +54,30 @@ __global__ void k_minmax(int64_t n, int d, const double *__restrict__ pts, unsig
         atomicMax(&mm[3 + threadIdx.x], shi[threadIdx.x]);
     }
 }
+__global__ void k_sum_i32(int64_t n, const int32_t *__restrict__ v, unsigned long long *out) {
+    unsigned long long t = 0;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT)
+        t += (unsigned long long)(unsigned)v[i];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, t);
+}
 }  // namespace
+
+// sum of n non-negative int32 values (host result)
+int64_t sum_i32(const int32_t *v, int64_t n, cudaStream_t st) {
+    unsigned long long *d = nullptr, h = 0;
+    MSK_CUDA(cudaMallocAsync((void **)&d, sizeof h, st));
+    MSK_CUDA(cudaMemsetAsync(d, 0, sizeof h, st));
+    if (n > 0) {
+        const int64_t nb = (n + NT - 1) / NT;
+        k_sum_i32<<<(unsigned)(nb < 1184 ? nb : 1184), NT, 0, st>>>(n, v, d);
+        MSK_CHECK_LAUNCH();
+    }
+    MSK_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st));
+    MSK_CUDA(cudaStreamSynchronize(st));
+    MSK_CUDA(cudaFreeAsync(d, st));
+    return (int64_t)h;
+}
 
 void minmax_points(int64_t n, int d, const double *pts, unsigned long long *mm, cudaStream_t st,
                    int *launches) {

@@ -37,7 +37,7 @@ CASES = [  # (name, hierarchy, T, patch_R, flags of the rank contexts' hierarchi
     ("halton3d-T3", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 3.0, 0.0, DIST_ALL),
     ("C3P4-T2", lambda: config("C3P4", m_eval=0), 2.0, 0.0, DIST_ALL),
     ("halton3d-T3-patch", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 3.0, 9.0, DIST_ALL),
-    # bench.py's setting (no DIST_ALL): only the 1.25M-point level (>= 2^20) is partitioned
+    # bench.py's setting (no DIST_ALL): the latency model partitions only the 1.25M-point level
     ("C3P5-default", lambda: config("C3P5", m_eval=0), 0.0, 0.0, 0),
     # the LITERAL schedule (Algorithm 2 as printed) with partitioned levels
     ("halton3d-literal", lambda: halton_hierarchy("h3", 3, [301, 2411, 9999], 1.5), 0.0, 0.0, DIST_ALL),

@@ -55,7 +55,7 @@ def test_rank_threads_equal_single_gpu_bitwise(world):
 
 @pytest.mark.gpu
 def test_rank_threads_full_size_bench_configuration():
-    """C3 as bench.py --gpus 2 runs it (levels >= 2^20 points partitioned:
+    """C3 as bench.py --gpus 2 runs it (the levels the latency model partitions:
     the 1.25M and 10M levels), 10^6 evaluation points: both ranks bit-identical
     to the single-GPU solve."""
     lib = build_shim()
