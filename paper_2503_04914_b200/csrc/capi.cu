@@ -363,8 +363,8 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     MSK_CUDA(cudaMemcpyAsync(hcptr.data(), cptr, sizeof(int64_t) * (ncols + 1), cudaMemcpyDeviceToHost, st));
     int *dstat = dalloc<int>(2, st);
     MSK_CUDA(cudaMemsetAsync(dstat, 0, 2 * sizeof(int), st));
-    int *pstat = dalloc<int>(5, st);  // patch path: CG failures, overflows, max iterations, max patch, count
-    MSK_CUDA(cudaMemsetAsync(pstat, 0, 5 * sizeof(int), st));
+    int *pstat = dalloc<int>(6, st);  // patch path: CG failures, overflows, max iterations, max patch, count x 2
+    MSK_CUDA(cudaMemsetAsync(pstat, 0, 6 * sizeof(int), st));
     MSK_CUDA(cudaStreamSynchronize(st));
     // ---- Lagrange columns, level by level, rounds of concurrent 32-column batches
     const int resident = 4 * 148;
@@ -398,18 +398,22 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             }
             pa.val_out = h->tval;
             pa.fail = pstat;
-            patch_count(pa, pstat + 4, st);
-            std::vector<int32_t> hc((size_t)D.n);
-            int hp = 0;
-            MSK_CUDA(cudaMemcpyAsync(&hp, pstat + 4, sizeof hp, cudaMemcpyDeviceToHost, st));
-            MSK_CUDA(cudaMemcpyAsync(hc.data(), D.cnt, sizeof(int32_t) * (size_t)D.n, cudaMemcpyDeviceToHost, st));
+            MSK_CUDA(cudaMemsetAsync(pstat + 4, 0, 2 * sizeof(int), st));
+            patch_count(pa, D.cnt, pstat + 4, st);  // [4] max patch points, [5] max sum of their row lengths
+            int hpz[2] = {0, 0};
+            MSK_CUDA(cudaMemcpyAsync(hpz, pstat + 4, sizeof hpz, cudaMemcpyDeviceToHost, st));
             MSK_CUDA(cudaStreamSynchronize(st));
-            const int maxrow = D.n ? *std::max_element(hc.begin(), hc.end()) : 0;
+            const int hp = hpz[0];
             if (getenv("MSK_DEBUG_PATCH"))
-                fprintf(stderr, "[msk] patch level %d: n %lld q %.6g rho %.6g reach %d cell %.6g pmax %d maxrow %d\n", l,
-                        (long long)D.n, D.q, rho, pa.reach, 1.0 / D.g.inv_cell, hp, maxrow);
+                fprintf(stderr, "[msk] patch level %d: n %lld q %.6g rho %.6g reach %d cell %.6g pmax %d nnz bound %d\n",
+                        l, (long long)D.n, D.q, rho, pa.reach, 1.0 / D.g.inv_cell, hp, hpz[1]);
+            if (hp > 65535)
+                throw Error(MSK_ERR_INVALID, "msk_assemble: local patch of " + std::to_string(hp) +
+                                                 " points (> 65535); reduce patch_R");
             pa.pmax = hp;
-            pa.nnzmax = (int)std::min<int64_t>((int64_t)hp * maxrow, (int64_t)hp * hp);
+            // the members' row lengths bound the patch-local entries (the workspace, and
+            // with it the CTAs per SM, is sized by it instead of pmax x max row length)
+            pa.nnzmax = (int)std::min<int64_t>((int64_t)hpz[1], (int64_t)hp * hp);
             const size_t smem = patch_smem_bytes(pa.pmax, pa.nnzmax);
             // larger patches run from a global workspace (patch_lagrange); bound it
             if (smem > (size_t)1 << 30)
@@ -570,7 +574,9 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
     for (int l = 0; l < h->L; ++l) {
         LevelData &D = h->lev[l];
         dfree(D.row_ptr, st); dfree(D.col, st); dfree(D.val, st); dfree(D.col16, st); dfree(D.cbase, st);
+        dfree(D.clen, st);
         D.row_ptr = nullptr; D.col = nullptr; D.val = nullptr; D.col16 = nullptr; D.cbase = nullptr;
+        D.clen = nullptr;
         nnz[l] = 0;
         D.nnz = 0;  // (partitioned levels accumulate their partitions' entries below)
         if (h->dist[l].on) {  // owned rows only, per local partition
@@ -671,17 +677,25 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
         // of 12).  Off by default: same-box A/B C3 finest level 40.1 vs
         // 32.7 ms, C2 21.3 vs 19.4 ms -- the decode lengthens the gather's address chain,
         // and the SpMV pass is gather-latency bound, not bandwidth bound
+        // The same per-chunk column windows serve k_cg's L2 prefetch of the next
+        // chunk's gathered r (MSK_RPREF=0: off).
         static const bool c16 = getenv("MSK_COL16") && getenv("MSK_COL16")[0] == '1';
-        if (c16 && D.n >= 256) {
+        static const bool rpref = !(getenv("MSK_RPREF") && getenv("MSK_RPREF")[0] == '0');
+        if ((c16 || rpref) && D.n >= 256) {
             const int CH = cg_chunk_tiles(D.n);
             const int64_t nch = ((D.n + 255) / 256 + CH - 1) / CH;
-            D.col16 = dalloc<uint16_t>((size_t)D.nnz + 16, st);
+            if (c16) {
+                D.col16 = dalloc<uint16_t>((size_t)D.nnz + 16, st);
+                MSK_CUDA(cudaMemsetAsync(D.col16 + D.nnz, 0, 16 * sizeof(uint16_t), st));
+            }
             D.cbase = dalloc<int4>((size_t)nch, st);
-            MSK_CUDA(cudaMemsetAsync(D.col16 + D.nnz, 0, 16 * sizeof(uint16_t), st));
+            if (rpref) D.clen = dalloc<int4>((size_t)nch, st);
             launches += 1;
-            if (!col16_build(D.n, D.row_ptr, D.col, D.col16, D.cbase, st)) {
-                dfree(D.col16, st); dfree(D.cbase, st);
-                D.col16 = nullptr; D.cbase = nullptr;
+            if (!col16_build(D.n, D.row_ptr, D.col, D.col16, D.cbase, D.clen, st)) {
+                // some chunk spans more than 4 windows: no 16-bit stream (the windows
+                // still steer the prefetch)
+                dfree(D.col16, st);
+                D.col16 = nullptr;
             }
         }
     }

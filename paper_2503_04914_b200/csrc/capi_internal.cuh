@@ -60,6 +60,7 @@ struct LevelData {
     double *val = nullptr;
     uint16_t *col16 = nullptr;     // 16-bit columns for k_cg (cg.cu col16_build), or null
     int4 *cbase = nullptr;         //   their window bases per reduction chunk
+    int4 *clen = nullptr;          //   and the extents (k_cg's L2 prefetch of the gathered r)
     double *alpha = nullptr;       // coefficients of the last solve, spatial order
     double4 *rec = nullptr;        // packed (coords, coefficient) records for gathers
     float4 *frec = nullptr;        // FP32 coordinates relative to lo (gather prefilter)
@@ -370,7 +371,7 @@ struct msk_hierarchy {
             LevelData &D = lev[l];
             dfree(D.xs, s); dfree(D.perm, s); dfree(D.cell_start, s); dfree(D.cnt, s);
             dfree(D.row_ptr, s); dfree(D.col, s); dfree(D.val, s); dfree(D.alpha, s); dfree(D.rec, s); dfree(D.frec, s);
-            dfree(D.col16, s); dfree(D.cbase, s);
+            dfree(D.col16, s); dfree(D.cbase, s); dfree(D.clen, s);
             D = LevelData();
         }
         dfree(ws, s);

@@ -23,6 +23,7 @@ CGLevelArgs cg_args(msk_hierarchy *h, int l, double tol, int max_iter, const dou
     a.val = D.val;
     a.col16 = D.col16;
     a.cbase = D.cbase;
+    a.clen = D.clen;
     a.b = b;
     a.b_src = b_src;
     a.b_perm = b_src ? D.perm : nullptr;
@@ -410,6 +411,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
             A.L.val = P.val;
             A.L.col16 = nullptr;
             A.L.cbase = nullptr;
+            A.L.clen = nullptr;
             A.L.nnz = P.nnz;
             A.L.chunk_tiles = CH;
             A.c0 = P.c0;

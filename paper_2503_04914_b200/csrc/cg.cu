@@ -273,6 +273,20 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
         const uint32_t cs = ps.CS + (uint32_t)k;
         // the epilogue's own-row vectors of the NEXT chunk -> L2 (hidden behind
         // this chunk's pieces; 33.38 -> 33.1 ms on the C3 finest level)
+        if (!PLAIN && tid == 0 && L.clen && k + 1 < K) {
+            // the next chunk's gathered r: its column windows -> L2 (r was written by
+            // every CTA in the last pass and competes with the streamed CSR for L2)
+            const int64_t cn = cbase + me + (k + 1) * nb;
+            const int4 b = __ldg(&L.cbase[cn]), e = __ldg(&L.clen[cn]);
+            const int bb[4] = {b.x, b.y, b.z, b.w}, ee[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                if (ee[w] <= 0) continue;
+                const uintptr_t a0 = (uintptr_t)(rv + bb[w]) & ~(uintptr_t)15;
+                const uintptr_t a1 = ((uintptr_t)(rv + bb[w] + ee[w]) + 15) & ~(uintptr_t)15;
+                prefetch_l2((const void *)a0, (uint32_t)(a1 - a0));
+            }
+        }
         if (!PLAIN && tid == 0 && !first && k + 1 < K) {
             int64_t nr0;
             int nrows;
@@ -1671,7 +1685,8 @@ unsigned dcg_grid(const DistCGArgs &a, int per_sm) {
 // per x-offset of its rows' cells), entry = window << 14 | (column - base).
 __global__ void __launch_bounds__(NT) k_col16(int64_t n, int CH, const int64_t *__restrict__ rp,
                                               const int32_t *__restrict__ col, uint16_t *__restrict__ col16,
-                                              int4 *__restrict__ cbase, int *__restrict__ fail) {
+                                              int4 *__restrict__ cbase, int4 *__restrict__ clen,
+                                              int *__restrict__ fail) {
     __shared__ int red[NW];
     const int64_t c = blockIdx.x;
     const int64_t r0 = c * CH * NT, r1 = r0 + (int64_t)CH * NT < n ? r0 + (int64_t)CH * NT : n;
@@ -1699,6 +1714,7 @@ __global__ void __launch_bounds__(NT) k_col16(int64_t n, int CH, const int64_t *
         base[w] = m;
         lower = (int64_t)m + 16384;
     }
+    int ext[4] = {0, 0, 0, 0};  // per window: largest offset + 1 (the extent read by the gathers)
     for (int64_t e = e0 + tid; e < e1; e += NT) {
         const int v = col[e];
         const int w = (v >= base[1]) + (v >= base[2]) + (v >= base[3]);
@@ -1707,9 +1723,14 @@ __global__ void __launch_bounds__(NT) k_col16(int64_t n, int CH, const int64_t *
             atomicOr(fail, 1);
             continue;
         }
-        col16[e] = (uint16_t)((w << 14) | (int)off);
+        ext[w] = (int)off + 1 > ext[w] ? (int)off + 1 : ext[w];
+        if (col16) col16[e] = (uint16_t)((w << 14) | (int)off);
     }
-    if (tid == 0) cbase[c] = make_int4(base[0], base[1], base[2], base[3]);
+    for (int w = 0; w < 4; ++w) ext[w] = -block_min(-ext[w]);
+    if (tid == 0) {
+        cbase[c] = make_int4(base[0], base[1], base[2], base[3]);
+        if (clen) clen[c] = make_int4(ext[0], ext[1], ext[2], ext[3]);
+    }
 }
 
 // co-resident CTAs of k_pcg's variant for a level (the per-rank grid is
@@ -1732,14 +1753,14 @@ void pcg_launch(const PeerCGArgs &a, cudaStream_t st) {
 }
 
 bool col16_build(int64_t n, const int64_t *row_ptr, const int32_t *col, uint16_t *col16, int4 *cbase,
-                 cudaStream_t st) {
+                 int4 *clen, cudaStream_t st) {
     if (n <= 0) return false;
     const int CH = cg_chunk_tiles(n);
     const int64_t nch = ((n + NT - 1) / NT + CH - 1) / CH;
     int *fail = nullptr, hf = 0;
     MSK_CUDA(cudaMallocAsync((void **)&fail, sizeof(int), st));
     MSK_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), st));
-    k_col16<<<(unsigned)nch, NT, 0, st>>>(n, CH, row_ptr, col, col16, cbase, fail);
+    k_col16<<<(unsigned)nch, NT, 0, st>>>(n, CH, row_ptr, col, col16, cbase, clen, fail);
     MSK_CHECK_LAUNCH();
     MSK_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaStreamSynchronize(st));

@@ -137,6 +137,7 @@ struct CGLevelArgs {
     // column = cbase[chunk].{x,y,z,w}[window] + offset; k_cg streams these instead of col
     const uint16_t *col16;
     const int4 *cbase;        // per reduction chunk (chunk_tiles * 256 rows): 4 window bases
+    const int4 *clen;         //   and the extents the chunk's columns span (L2 prefetch of r), or null
 };
 // ---- multi-RHS CG (msk_solve_multi; cg.cu): one level, R right-hand sides
 // with their own scalars; per column the arithmetic of k_cg (bit-identical to
@@ -209,7 +210,7 @@ int cg_max_resident_blocks();
 // stream): returns false (and writes nothing usable) when some chunk's columns
 // need more than 4 windows of 2^14 indices
 bool col16_build(int64_t n, const int64_t *row_ptr, const int32_t *col, uint16_t *col16, int4 *cbase,
-                 cudaStream_t st);
+                 int4 *clen, cudaStream_t st);
 
 // ---- partitioned CG over peer memory (cg.cu k_pcg): the
 // whole CG of a row-partitioned level in ONE persistent launch per rank.
@@ -333,8 +334,9 @@ struct PatchArgs {
     double *val_out;                // factor values
     int *fail;                      // [0] CG failures, [1] patch overflows, [2] max iterations, [3] max patch
 };
-// max patch size over the columns (count pass, exact test) into *pmax_out (device int)
-void patch_count(const PatchArgs &a, int *pmax_out, cudaStream_t st);
+// max patch size over the columns (count pass, exact test) into pmax_out[0] and the max
+// sum of the members' row lengths of A_l (rowcnt; bounds the patch-local entries) into [1]
+void patch_count(const PatchArgs &a, const int32_t *rowcnt, int *pmax_out, cudaStream_t st);
 void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launches);
 size_t patch_smem_bytes(int pmax, int nnzmax);
 // out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)

@@ -274,7 +274,8 @@ size_t patch_smem_bytes_impl(int pmax, int nnzmax) {
     b = (b + 15) & ~(size_t)15;
     b += sizeof(double) * 4 * (size_t)pmax;       // x r p q
     b += sizeof(double) * (size_t)nnzmax;         // pval
-    b += sizeof(int32_t) * (size_t)nnzmax;        // pcol
+    b += sizeof(uint16_t) * (size_t)nnzmax;       // pcol (patch-local, < 65536 points)
+    b = (b + 15) & ~(size_t)15;
     b += sizeof(int32_t) * 1024;                  // column counts / scan scratch
     return b + 64;
 }
@@ -310,8 +311,11 @@ __device__ __forceinline__ void patch_range(const LevelView &L, int q, int64_t x
     e = L.cell_start[kb + z1 + 1];
 }
 
+// per column: the patch size and the sum of its members' row lengths in A_l
+// (an upper bound of the patch-local nonzeros) -> maxima in pmax_out[0], [1]
 template <int D>
-__global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, int *pmax_out) {
+__global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, const int32_t *__restrict__ rowcnt,
+                                                    int *pmax_out) {
     const int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
     if (i >= a.ncols) return;
     const LevelView &L = a.Lv;
@@ -319,15 +323,20 @@ __global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, int *pmax_out) 
 #pragma unroll
     for (int t = 0; t < D; ++t) x[t] = L.x[t][i];
     int cnt = 0;
+    long long nz = 0;
     for_each_range_m<D>(L, x, a.reach, [&](int b, int e) {
         for (int h = b; h < e; ++h) {
             double y[3];
 #pragma unroll
             for (int t = 0; t < D; ++t) y[t] = L.x[t][h];
-            if (dist2_nofma<D>(x, y) < a.rho2) ++cnt;
+            if (dist2_nofma<D>(x, y) < a.rho2) {
+                ++cnt;
+                nz += rowcnt[h];
+            }
         }
     });
     atomicMax(pmax_out, cnt);
+    atomicMax(pmax_out + 1, (int)(nz < 0x7fffffffll ? nz : 0x7fffffffll));
 }
 
 __device__ __forceinline__ int find_sorted(const int32_t *v, int n, int32_t key) {
@@ -392,8 +401,8 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     double *X = reinterpret_cast<double *>(ptr);
     double *Rv = X + pmax, *P = Rv + pmax, *Q = P + pmax;
     double *pval = Q + pmax;
-    int32_t *pcol = reinterpret_cast<int32_t *>(pval + a.nnzmax);
-    int32_t *ccnt = pcol + a.nnzmax;  // 1024 column counters
+    uint16_t *pcol = reinterpret_cast<uint16_t *>(pval + a.nnzmax);
+    int32_t *ccnt = reinterpret_cast<int32_t *>(((uintptr_t)(pcol + a.nnzmax) + 15) & ~(uintptr_t)15);  // 1024 counters
     double xc[3];
 #pragma unroll
     for (int t = 0; t < D; ++t) xc[t] = L.x[t][i];
@@ -459,7 +468,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k) {
             const int lc = find_sorted(pid, np, a.col[k]);
             if (lc >= 0) {
-                pcol[w] = lc;
+                pcol[w] = (uint16_t)lc;
                 pval[w] = a.val[k];
                 ++w;
             }
@@ -548,10 +557,10 @@ __global__ void __launch_bounds__(NT) k_patch(PatchArgs a, unsigned char *gws, s
 
 size_t patch_smem_bytes(int pmax, int nnzmax) { return patch_smem_bytes_impl(pmax, nnzmax); }
 
-void patch_count(const PatchArgs &a, int *pmax_out, cudaStream_t st) {
+void patch_count(const PatchArgs &a, const int32_t *rowcnt, int *pmax_out, cudaStream_t st) {
     if (a.ncols <= 0) return;
-    if (a.d == 2) k_patch_count<2><<<ceil_div_u(a.ncols, NT), NT, 0, st>>>(a, pmax_out);
-    else k_patch_count<3><<<ceil_div_u(a.ncols, NT), NT, 0, st>>>(a, pmax_out);
+    if (a.d == 2) k_patch_count<2><<<ceil_div_u(a.ncols, NT), NT, 0, st>>>(a, rowcnt, pmax_out);
+    else k_patch_count<3><<<ceil_div_u(a.ncols, NT), NT, 0, st>>>(a, rowcnt, pmax_out);
     MSK_CHECK_LAUNCH();
 }
 
