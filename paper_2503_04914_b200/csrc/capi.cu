@@ -677,10 +677,11 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
         // of 12).  Off by default: same-box A/B C3 finest level 40.1 vs
         // 32.7 ms, C2 21.3 vs 19.4 ms -- the decode lengthens the gather's address chain,
         // and the SpMV pass is gather-latency bound, not bandwidth bound
-        // The same per-chunk column windows serve k_cg's L2 prefetch of the next
-        // chunk's gathered r (MSK_RPREF=0: off).
+        // The same per-chunk column windows can steer an L2 prefetch of the next chunk's
+        // gathered r (MSK_RPREF=1).  Off by default: same-box A/B, C3 finest 32.91 ms
+        // either way, level 5 3.46 vs 3.33 ms (the gathered r already hits L2).
         static const bool c16 = getenv("MSK_COL16") && getenv("MSK_COL16")[0] == '1';
-        static const bool rpref = !(getenv("MSK_RPREF") && getenv("MSK_RPREF")[0] == '0');
+        static const bool rpref = getenv("MSK_RPREF") && getenv("MSK_RPREF")[0] == '1';
         if ((c16 || rpref) && D.n >= 256) {
             const int CH = cg_chunk_tiles(D.n);
             const int64_t nch = ((D.n + 255) / 256 + CH - 1) / CH;
