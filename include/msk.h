@@ -346,11 +346,12 @@ MSK_API msk_status msk_export_cells(msk_hierarchy *h, int level, int32_t *perm, 
                             int64_t *cell_key, double *lo, double *cell, int64_t *dims);
 
 /* The exact grid of level l (a1; reading C-26): origin lo [host] d doubles,
- * inv_cell [host] 1 double -- the FP64 factor of the key map, so a point's
- * cell coordinate along axis a is floor((x_a - lo_a) * inv_cell) with one
- * rounded subtraction and one rounded multiplication (no FMA, reading C-4),
- * clamped to [0, dims_a - 1] -- and dims [host] d int64.  Any output may be
- * NULL.  MSK_ERR_INVALID for a bad level. */
+ * inv_cell [host] d doubles -- the FP64 factors of the key map per axis, so a
+ * point's cell coordinate along axis a is floor((x_a - lo_a) * inv_cell[a])
+ * with one rounded subtraction and one rounded multiplication (no FMA, reading
+ * C-4), clamped to [0, dims_a - 1]; the last axis has cells zf times thinner
+ * (inv_cell[d-1] = zf inv_cell[0], zf a power of two) -- and dims [host] d
+ * int64.  Any output may be NULL.  MSK_ERR_INVALID for a bad level. */
 MSK_API msk_status msk_export_grid(msk_hierarchy *h, int level, double *lo, double *inv_cell, int64_t *dims);
 
 /* y = B_{row_level,col_level} v (a3).  row_level == col_level uses the

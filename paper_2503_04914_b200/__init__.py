@@ -400,10 +400,10 @@ class Hierarchy:
         cell = np.zeros(1)
         dims = np.zeros(3, dtype=np.int64)
         msk_export_cells(self.handle, level, perm, cs, keys, lo, cell, dims)
-        inv = np.zeros(1)
+        inv = np.zeros(3)
         msk_export_grid(self.handle, level, None, inv, None)
         return dict(perm=perm, cell_start=cs, keys=keys, lo=lo[:self.d], cell=float(cell[0]),
-                    inv_cell=float(inv[0]), dims=dims[:self.d])
+                    inv_cell=inv[:self.d].copy(), dims=dims[:self.d])
 
     def apply_block(self, row_level: int, col_level: int, v, y=None):
         v = _f64(v)

@@ -116,6 +116,16 @@ extern "C" msk_status msk_partition_rows(int64_t n, int world, int64_t *bounds) 
     API_END
 }
 
+// Refinement of the last grid axis (Grid::zf): MSK_ZF (1, 2, 4, 8; default 4).
+int grid_zf() {
+    static const int zf = [] {
+        const char *e = getenv("MSK_ZF");
+        const int v = e ? atoi(e) : 4;
+        return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+    }();
+    return zf;
+}
+
 // =============================================================== hierarchy
 extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int64_t *n,
                                            const double *const *points, const double *delta,
@@ -175,23 +185,28 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
             D.delta = delta[l];
             h->off[l + 1] = h->off[l] + n[l];
             double cell = delta[l] * (1.0 + 0x1p-20);
+            const int zf = grid_zf();
             for (;;) {
                 // the cell count is formed in double first: extent / delta can be
                 // large enough (3-D, > ~2.6e6 per axis) to overflow int64 products
-                double dims_d[3], ncells_d = 1.0;
+                const double inv = 1.0 / cell;
+                double invs[3], dims_d[3], ncells_d = 1.0;
                 for (int a = 0; a < 3; ++a) {
-                    dims_d[a] = a < d ? floor((h->hi[a] - h->lo[a]) * (1.0 / cell)) + 1.0 : 1.0;
+                    invs[a] = a == d - 1 ? (double)zf * inv : inv;  // exact: zf is a power of two
+                    dims_d[a] = a < d ? floor((h->hi[a] - h->lo[a]) * invs[a]) + 1.0 : 1.0;
                     ncells_d *= dims_d[a];
                 }
                 require(std::isfinite(ncells_d), "msk_hierarchy_create: non-finite cell grid");
                 // bound the cell count (points much sparser than delta): larger
                 // cells only add candidates, never lose neighbours
-                if (ncells_d <= 8.0 * (double)n[l] + 4096.0) {
+                if (ncells_d <= (double)zf * (8.0 * (double)n[l] + 4096.0)) {
                     Grid g{};
-                    g.inv_cell = 1.0 / cell;
+                    g.inv_cell = inv;
+                    g.zf = zf;
                     g.ncells = 1;
                     for (int a = 0; a < 3; ++a) {
                         g.lo[a] = a < d ? h->lo[a] : 0.0;
+                        g.inv[a] = invs[a];
                         g.dim[a] = (int64_t)dims_d[a];
                         g.ncells *= g.dim[a];
                     }
@@ -873,8 +888,8 @@ extern "C" msk_status msk_export_grid(msk_hierarchy *h, int level, double *lo, d
     for (int a = 0; a < h->d; ++a) {
         if (lo) lo[a] = D.g.lo[a];
         if (dims) dims[a] = D.g.dim[a];
+        if (inv_cell) inv_cell[a] = D.g.inv[a];
     }
-    if (inv_cell) *inv_cell = D.g.inv_cell;
     API_END
 }
 

@@ -62,14 +62,19 @@ inline void debug_sync(cudaStream_t st, const char *what) {
 constexpr int kMaxLevels = 16;
 
 // ---------------------------------------------------------------- geometry
-// Uniform grid of one level: cell side c >= delta (1 + 2^-20), row-major
-// x-major keys key = (ix * ny + iy) * nz + iz (nz = 1 in 2-D).  A pair with
-// r < delta lies in cells whose indices differ by at most 1 per axis
-// (DESIGN.md "Cell list").
+// Grid of one level: cell side c >= delta (1 + 2^-20) along the leading axes
+// and c / zf along the LAST axis (z in 3-D, y in 2-D; zf a power of two, so
+// inv[last] = zf * inv_cell exactly); row-major x-major keys key = (ix * ny +
+// iy) * nz + iz (nz = 1 in 2-D).  A pair with r < delta lies in cells whose
+// indices differ by at most 1 along the leading axes and by at most zf along
+// the last one (the thin last-axis cells trim each of
+// the 3^(d-1) contiguous candidate ranges from 3 delta to (2 zf + 1) delta / zf).
 struct Grid {
     double lo[3];
-    double inv_cell;
-    int64_t dim[3];  // nx, ny, nz (nz = 1 for d = 2)
+    double inv_cell;  // 1 / c (leading axes)
+    double inv[3];    // per axis: inv_cell, or zf * inv_cell on the last axis
+    int zf;           // last-axis refinement (1 = cubic cells)
+    int64_t dim[3];   // nx, ny, nz (nz = 1 for d = 2)
     int64_t ncells;
 };
 
@@ -118,7 +123,7 @@ __device__ __forceinline__ double wendland(double r) {
 
 // cell coordinate of x along axis a, not clamped
 __device__ __forceinline__ int64_t cell_coord(const Grid &g, int a, double x) {
-    return (int64_t)floor(__dmul_rn(__dsub_rn(x, g.lo[a]), g.inv_cell));
+    return (int64_t)floor(__dmul_rn(__dsub_rn(x, g.lo[a]), g.inv[a]));
 }
 
 // --------------------------------------------------------- reductions

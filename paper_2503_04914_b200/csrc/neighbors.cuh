@@ -1,8 +1,8 @@
 // neighbors.cuh -- candidate enumeration over a level's cell list.
 //
 // For a target x, the candidates are the points of the cells whose indices
-// differ from x's (unclamped) cell by at most one per axis, intersected with
-// the grid.  With row-major keys the cells along the last axis are
+// differ from x's (unclamped) cell by at most one along the leading axes and
+// at most zf along the last (thin) axis, intersected with the grid.  With row-major keys the cells along the last axis are
 // contiguous, so a 3-D query is 9 contiguous ranges and a 2-D query 3.
 // Visiting ranges in increasing key order yields candidates in increasing
 // spatial index.
@@ -16,9 +16,9 @@ __device__ __forceinline__ void for_each_range(const LevelView &L, const double 
     int64_t c[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) c[a] = cell_coord(L.g, a, x[a]);
-    const int64_t la = D - 1;
-    int64_t lo_last = c[la] - 1 < 0 ? 0 : c[la] - 1;
-    int64_t hi_last = c[la] + 1 >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + 1;
+    const int64_t la = D - 1, z = L.g.zf;  // last axis: zf thin cells span delta
+    int64_t lo_last = c[la] - z < 0 ? 0 : c[la] - z;
+    int64_t hi_last = c[la] + z >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + z;
     if (lo_last > hi_last) return;
     int64_t x0 = c[0] - 1 < 0 ? 0 : c[0] - 1;
     int64_t x1 = c[0] + 1 >= L.g.dim[0] ? L.g.dim[0] - 1 : c[0] + 1;
@@ -103,17 +103,18 @@ __device__ __forceinline__ void for_each_hit(const LevelView &cols, const double
     flush();
 }
 
-// Same enumeration with a reach of m cells per axis (radius up to m cell
-// sides): used for the truncation radius T q_l of the thresholded factor,
-// which spans several cells of the level grid.
+// Same enumeration with a reach of m cells along the leading axes (radius
+// below m cell sides) and m * zf thin cells along the last one: used for the
+// truncation radius T q_l of the thresholded factor, which spans several cells
+// of the level grid.
 template <int D, typename F>
 __device__ __forceinline__ void for_each_range_m(const LevelView &L, const double *x, int m, F &&f) {
     int64_t c[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) c[a] = cell_coord(L.g, a, x[a]);
-    const int64_t la = D - 1;
-    int64_t lo_last = c[la] - m < 0 ? 0 : c[la] - m;
-    int64_t hi_last = c[la] + m >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + m;
+    const int64_t la = D - 1, mz = (int64_t)m * L.g.zf;
+    int64_t lo_last = c[la] - mz < 0 ? 0 : c[la] - mz;
+    int64_t hi_last = c[la] + mz >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + mz;
     if (lo_last > hi_last) return;
     int64_t x0 = c[0] - m < 0 ? 0 : c[0] - m;
     int64_t x1 = c[0] + m >= L.g.dim[0] ? L.g.dim[0] - 1 : c[0] + m;

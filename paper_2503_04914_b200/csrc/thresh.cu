@@ -287,8 +287,9 @@ __device__ __forceinline__ void patch_columns(const LevelView &L, const double *
 #pragma unroll
     for (int a = 0; a < D; ++a) c[a] = cell_coord(L.g, a, x[a]);
     const int la = D - 1;
-    z0 = c[la] - m < 0 ? 0 : c[la] - m;
-    z1 = c[la] + m >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + m;
+    const int64_t mz = (int64_t)m * L.g.zf;  // thin last-axis cells
+    z0 = c[la] - mz < 0 ? 0 : c[la] - mz;
+    z1 = c[la] + mz >= L.g.dim[la] ? L.g.dim[la] - 1 : c[la] + mz;
     x0 = c[0] - m < 0 ? 0 : c[0] - m;
     x1 = c[0] + m >= L.g.dim[0] ? L.g.dim[0] - 1 : c[0] + m;
     if (D == 3) {

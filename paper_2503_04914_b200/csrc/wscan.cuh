@@ -84,8 +84,9 @@ __device__ __forceinline__ void scan_level(const LevelView &L, const double *x, 
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             const int64_t c = cell_coord(L.g, a, x[a]);
-            const int64_t l = c - 1 < 0 ? 0 : c - 1;
-            const int64_t h = c + 1 >= L.g.dim[a] ? L.g.dim[a] - 1 : c + 1;
+            const int64_t rr = a == D - 1 ? L.g.zf : 1;  // thin last-axis cells
+            const int64_t l = c - rr < 0 ? 0 : c - rr;
+            const int64_t h = c + rr >= L.g.dim[a] ? L.g.dim[a] - 1 : c + rr;
             if (l > h) valid = false;
             else { lo[a] = (int)l; hi[a] = (int)h; }
         }

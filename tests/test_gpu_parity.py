@@ -69,10 +69,11 @@ HIERS = {
 # --------------------------------------------------------------- a1 cell list
 def _assert_keys_exact(P, c):
     """Every sorted point's key equals the key map recomputed here from the
-    exported grid: floor((x - lo) * inv_cell) with one rounded subtraction and
-    one rounded multiplication (numpy evaluates each ufunc separately, so no
-    FMA: reading C-4), clamped to the grid, row-major x-major (reading C-26).
-    Bit-exact, no tolerance."""
+    exported grid: floor((x_a - lo_a) * inv_cell[a]) per axis with one rounded
+    subtraction and one rounded multiplication (numpy evaluates each ufunc
+    separately, so no FMA: reading C-4), clamped to the grid, row-major
+    x-major (reading C-26); the last axis has thin cells (inv_cell[-1] = zf x
+    inv_cell[0], zf a power of two).  Bit-exact, no tolerance."""
     Ps = P[c["perm"]]
     dims = np.asarray(c["dims"], dtype=np.int64)
     cc = np.floor((Ps - np.asarray(c["lo"])) * c["inv_cell"]).astype(np.int64)
@@ -81,8 +82,11 @@ def _assert_keys_exact(P, c):
     for a in range(1, P.shape[1]):
         key = key * dims[a] + cc[:, a]
     assert np.array_equal(key, c["keys"])
-    # the key map is the grid the cell side describes
-    assert c["inv_cell"] == 1.0 / c["cell"] or abs(c["inv_cell"] * c["cell"] - 1.0) < 1e-15
+    # the key map is the grid the cell side describes; the last axis is refined by a power of two
+    inv = np.asarray(c["inv_cell"])
+    assert abs(inv[0] * c["cell"] - 1.0) < 1e-15 and np.all(inv[:-1] == inv[0])
+    zf = inv[-1] / inv[0]
+    assert zf in (1.0, 2.0, 4.0, 8.0)
 
 
 
