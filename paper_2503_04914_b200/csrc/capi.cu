@@ -116,12 +116,16 @@ extern "C" msk_status msk_partition_rows(int64_t n, int world, int64_t *bounds) 
     API_END
 }
 
-// Refinement of the last grid axis (Grid::zf): MSK_ZF (1, 2, 4, 8; default 4).
+// Refinement of the last grid axis (Grid::zf): MSK_ZF (1, 2, 4, 8; default 2).
+// Same-box A/B on C3: step 55.73 / 55.57 / 56.18 / 57.40 ms for
+// zf = 1 / 2 / 4 / 8 -- thinner cells trim the candidate ranges (B products
+// 5.56 -> 5.25 -> 5.14 ms) but multiply the cells the cell-list passes visit
+// (create 2.58 -> 2.78 -> 3.26 ms).
 int grid_zf() {
     static const int zf = [] {
         const char *e = getenv("MSK_ZF");
-        const int v = e ? atoi(e) : 4;
-        return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+        const int v = e ? atoi(e) : 2;
+        return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
     }();
     return zf;
 }
