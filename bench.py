@@ -38,6 +38,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# C4F: coarse levels above this many points get local-patch Lagrange functions
+# (C3: levels 3-6 -> 19,531 .. 1.25M columns; levels 1-2 exact).  Round 1 used
+# 20000 (level 3 exact: 609 ms of the 1.96 s build).
+PATCH_MIN_N = 4000
+
 METRIC = "multiscale solve time & Wendland nonzeros/s (GNNZ/s, % HBM roofline) at 1/2/4/8 B200"
 UNIT = "GNNZ/s"
 WORKLOAD = ("C3: d=3, 6 nested Halton(2,3,5) levels N=305..1e7 (round(1e7*8^(l-6))), "
@@ -135,7 +140,7 @@ def run_msk(args, rank, world, local_rank):
 
     def step(pts, f, xe, alpha, s):
         h = msk.Hierarchy(ctx, pts, H.delta, H.q, k=H.k, flags=hflags)
-        h.assemble(T=thr, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=20000)
+        h.assemble(T=thr, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=PATCH_MIN_N)
         _, sinfo = h.solve(f, tol=args.tol, max_iter=20000, schedule=sched, alpha=alpha)
         _, einfo = h.evaluate(xe, out=s)
         hinfo = h.info()
@@ -212,7 +217,7 @@ def run_msk(args, rank, world, local_rank):
         if rank == 0:
             c1 = msk.Context(local_rank, stream.cuda_stream)
             h1 = msk.Hierarchy(c1, pts_d, H.delta, H.q, k=H.k, flags=hflags)
-            h1.assemble(T=thr, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=20000)
+            h1.assemble(T=thr, lagrange_tol=1e-14, patch_R=patch_R, patch_min_n=PATCH_MIN_N)
             _, si1 = h1.solve(f_d, tol=args.tol, max_iter=20000, schedule=sched)
             _, ei1 = h1.evaluate(xe_d)
             nnz_all = e2e_nnz_all = nnz_of(h1.info(), si1, ei1)
@@ -431,7 +436,7 @@ def main():
                     help="T of the thresholded factor (C4 default 3; 0 = exact mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--patch-R", type=float, default=None,
-                    help="local-patch Lagrange radius (units of q_l) for levels > 20000 points (T > 0; C4F: 11)")
+                    help="local-patch Lagrange radius (units of q_l) for levels > 4000 points (T > 0; C4F: 11)")
     ap.add_argument("--matrix-free", action="store_true",
                     help="MSK_FLAG_MATRIX_FREE: A_l never stored, CG SpMVs evaluate Phi on the fly")
     args = ap.parse_args()

@@ -323,6 +323,18 @@ namespace {
 void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_R, int64_t patch_min_n,
                   int *launches) {
     cudaStream_t st = h->st();
+    // MSK_DEBUG_PATCH: device time of each phase of the build (stderr)
+    const bool dbg = getenv("MSK_DEBUG_PATCH") != nullptr;
+    std::vector<std::pair<std::string, Timer *>> ph;
+    auto mark = [&](const std::string &name) {
+        if (!dbg) return;
+        ph.emplace_back(name, new Timer(st));
+        ph.back().second->start();
+    };
+    auto done = [&]() {
+        if (!dbg || ph.empty()) return;
+        ph.back().second->stop();
+    };
     const int L = h->L, d = h->d;
     const int64_t ntot = h->ntot;
     // ---- pattern: rows = all points (level 0 rows empty), columns global
@@ -348,11 +360,13 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
         }
         return a;
     };
+    mark("pattern count");
     for (int k = 1; k < L; ++k) {
         ThreshPatternArgs a = pattern_args(k);
         a.cnt = cnt + h->off[k];
         thresh_count(a, st, launches);
     }
+    done();
     h->trow_ptr = dalloc<int64_t>((size_t)(ntot + 1), st);
     exclusive_scan_i64(cnt, ntot, h->trow_ptr, st, launches);
     int64_t nnz = 0;
@@ -363,6 +377,7 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     h->tcol = dalloc<int32_t>((size_t)nnz, st);
     h->tval = dalloc<double>((size_t)nnz, st);
     h->tbucket = dalloc<uint8_t>((size_t)nnz, st);
+    mark("pattern fill");
     for (int k = 1; k < L; ++k) {
         ThreshPatternArgs a = pattern_args(k);
         a.row_ptr = h->trow_ptr + h->off[k];
@@ -370,6 +385,8 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
         a.bucket = h->tbucket;
         thresh_fill(a, st, launches);
     }
+    done();
+    mark("transpose index");
     // ---- transpose index over the coarse columns (levels 0..L-2)
     const int64_t ncols = h->off[L - 1];
     int64_t *cptr = dalloc<int64_t>((size_t)(ncols + 1), st);
@@ -378,6 +395,7 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     int32_t *ccol = nullptr;  // columns are found by binary search in cptr (saves 4 B per entry)
     thresh_csc(ntot - h->off[1], h->off[1], nnz, ncols, h->trow_ptr, h->tcol, cptr, cpos, crow, ccol, st,
                launches);
+    done();
     std::vector<int64_t> hcptr((size_t)(ncols + 1));
     MSK_CUDA(cudaMemcpyAsync(hcptr.data(), cptr, sizeof(int64_t) * (ncols + 1), cudaMemcpyDeviceToHost, st));
     int *dstat = dalloc<int>(2, st);
@@ -438,7 +456,9 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             if (smem > (size_t)1 << 30)
                 throw Error(MSK_ERR_INVALID, "msk_assemble: local patch too large (" + std::to_string(hp) +
                                                  " points); reduce patch_R");
+            mark("level " + std::to_string(l) + " patches (k_patch)");
             patch_lagrange(pa, smem, st, launches);
+            done();
             MSK_CUDA(cudaMemsetAsync(pstat + 4, 0, sizeof(int), st));
             continue;
         }
@@ -461,7 +481,9 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             m.ws = ws;
             m.fail = dstat;
             m.max_iters = dstat + 1;
+            mark("level " + std::to_string(l) + " exact Lagrange CG");
             thresh_cg_multi(m, (int)nb, st, launches);
+            done();
             const int64_t c0 = b0 * 32, c1 = std::min<int64_t>((b0 + nb) * 32, D.n);
             ThreshValueArgs v{};
             v.d = d;
@@ -484,7 +506,9 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             v.Lv = h->view(l);
             v.ws = ws;
             v.val = h->tval;
+            mark("level " + std::to_string(l) + " values");
             thresh_values(v, st, launches);
+            done();
         }
         dfree(ws, st);
     }
@@ -493,6 +517,12 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
     MSK_CUDA(cudaMemcpyAsync(hps, pstat, sizeof hps, cudaMemcpyDeviceToHost, st));
     MSK_CUDA(cudaStreamSynchronize(st));
     dfree(dstat, st); dfree(pstat, st); dfree(cptr, st); dfree(cpos, st); dfree(crow, st); dfree(ccol, st);
+    if (dbg) {
+        for (auto &p : ph) {
+            fprintf(stderr, "[msk] factor build %-34s %9.3f ms\n", p.first.c_str(), p.second->ms());
+            delete p.second;
+        }
+    }
     h->lagrange_max_iters = std::max(hstat[1], hps[2]);
     h->patch_max_points = hps[3];
     if (hstat[0]) throw Error(MSK_ERR_NOCONV, "msk_assemble: Lagrange CG did not converge in 20000 iterations");

@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(NT) k_csc_spmv_add(int64_t ncols, const int64_
 size_t patch_smem_bytes_impl(int pmax, int nnzmax) {
     size_t b = 0;
     b += sizeof(int32_t) * (size_t)pmax;          // pid
-    b += sizeof(int32_t) * (size_t)(pmax + 1);    // prow
+    b += sizeof(int32_t) * (size_t)(pmax + 1);    // prow (row slots: starts)
+    b += sizeof(int32_t) * (size_t)pmax;          // pcnt (entries per row slot)
     b = (b + 15) & ~(size_t)15;
     b += sizeof(double) * 4 * (size_t)pmax;       // x r p q
     b += sizeof(double) * (size_t)nnzmax;         // pval
@@ -340,6 +341,25 @@ __global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, const int32_t *
     atomicMax(pmax_out + 1, (int)(nz < 0x7fffffffll ? nz : 0x7fffffffll));
 }
 
+// find_sorted for ascending keys: `pos` is the lower bound of the previous key;
+// a few linear steps from it (a row's columns, or a stored row's hits, come in
+// clusters of nearby global ids), else a binary search of the rest.  Returns
+// the index or -1 and leaves pos at key's lower bound.
+__device__ __forceinline__ int find_from(const int32_t *v, int n, int32_t key, int &pos) {
+    int lo = pos;
+    for (int s = 0; s < 4 && lo < n && v[lo] < key; ++s) ++lo;
+    if (lo < n && v[lo] < key) {
+        int hi = n;
+        ++lo;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (v[mid] < key) lo = mid + 1; else hi = mid;
+        }
+    }
+    pos = lo;
+    return lo < n && v[lo] == key ? lo : -1;
+}
+
 __device__ __forceinline__ int find_sorted(const int32_t *v, int n, int32_t key) {
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -384,11 +404,26 @@ __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp
     return total;
 }
 
+// Block sum with ONE barrier (the patch CG is barrier-latency bound: one CTA,
+// ~60 iterations of ~730 rows): warp xor-trees, the warp partials in `buf`,
+// every thread adds them in warp order (a fixed order: deterministic).  The
+// caller alternates two buffers, so a buffer is rewritten only after a later
+// barrier has retired its readers.
+__device__ __forceinline__ double block_sum_1bar(double v, double *buf) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) t += buf[w];
+    return t;
+}
+
 // one column; `base` = the CTA's workspace (shared memory, or a global slice
 // for patches that do not fit); every early return is CTA-uniform
 template <int D, int K>
 __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsigned char *base) {
-    __shared__ double red[NT / 32 + 2];
+    __shared__ double red1[NT / 32], red2[NT / 32];  // the two CG reductions alternate buffers
     __shared__ int32_t tmp[NT + 1];
     const int tid = threadIdx.x;
     const LevelView &L = a.Lv;
@@ -398,6 +433,8 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     ptr += sizeof(int32_t) * (size_t)pmax;
     int32_t *prow = reinterpret_cast<int32_t *>(ptr);
     ptr += sizeof(int32_t) * (size_t)(pmax + 1);
+    int32_t *pcnt = reinterpret_cast<int32_t *>(ptr);
+    ptr += sizeof(int32_t) * (size_t)pmax;
     ptr = reinterpret_cast<unsigned char *>(((uintptr_t)ptr + 15) & ~(uintptr_t)15);
     double *X = reinterpret_cast<double *>(ptr);
     double *Rv = X + pmax, *P = Rv + pmax, *Q = P + pmax;
@@ -444,36 +481,35 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     }
     __syncthreads();
     if (tid == 0) atomicMax(&a.fail[3], np);
-    // ---- 2. local CSR of A restricted to the patch
+    // ---- 2. local CSR of A restricted to the patch, in one pass: row r gets a
+    // slot of its full A_l row length (the slots fit: the workspace is sized by
+    // the largest sum of the members' row lengths), pcnt[r] of them are used
     for (int r = tid; r < np; r += NT) {
         const int32_t g = pid[r];
-        int n = 0;
-        for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k)
-            if (find_sorted(pid, np, a.col[k]) >= 0) ++n;
-        prow[r] = n;
+        prow[r] = (int32_t)(a.row_ptr[g + 1] - a.row_ptr[g]);
     }
     __syncthreads();
-    int nnz = 0;
+    int nslot = 0;
     {
-        // scan prow[0..np) (reuse block_scan_excl on the prow array)
-        nnz = block_scan_excl(prow, np, tmp);
-        if (tid == 0) prow[np] = nnz;
+        nslot = block_scan_excl(prow, np, tmp);
+        if (tid == 0) prow[np] = nslot;
     }
-    if (nnz > a.nnzmax) {
+    if (nslot > a.nnzmax) {
         if (tid == 0) atomicAdd(&a.fail[1], 1);
         return;
     }
     for (int r = tid; r < np; r += NT) {
         const int32_t g = pid[r];
-        int w = prow[r];
-        for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k) {
-            const int lc = find_sorted(pid, np, a.col[k]);
+        int w = prow[r], pos = 0;
+        for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k) {  // ascending columns
+            const int lc = find_from(pid, np, a.col[k], pos);
             if (lc >= 0) {
                 pcol[w] = (uint16_t)lc;
                 pval[w] = a.val[k];
                 ++w;
             }
         }
+        pcnt[r] = w - prow[r];
     }
     // ---- 3. CG on A_P c = e_center
     const int ctr = find_sorted(pid, np, (int32_t)i);
@@ -495,11 +531,12 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         double pq = 0.0;
         for (int r = tid; r < np; r += NT) {
             double acc = 0.0;
-            for (int k = prow[r]; k < prow[r + 1]; ++k) acc = fma(pval[k], P[pcol[k]], acc);
+            const int k0 = prow[r], k1 = k0 + pcnt[r];
+            for (int k = k0; k < k1; ++k) acc = fma(pval[k], P[pcol[k]], acc);
             Q[r] = acc;
             pq += P[r] * acc;
         }
-        pq = block_sum<NT>(pq, red);
+        pq = block_sum_1bar(pq, red1);
         const double alpha = rr / pq;
         double rn = 0.0;
         for (int r = tid; r < np; r += NT) {
@@ -508,7 +545,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
             rn += v * v;
             X[r] += alpha * P[r];
         }
-        rn = block_sum<NT>(rn, red);
+        rn = block_sum_1bar(rn, red2);
         const double beta = rn / rr;
         rr = rn;
         for (int r = tid; r < np; r += NT) P[r] = Rv[r] + beta * P[r];
@@ -529,6 +566,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
 #pragma unroll
         for (int q = 0; q < D; ++q) xj[q] = a.lev_xs[k][(int64_t)q * a.lev_n[k] + j];
         double s = 0.0;
+        int pos = 0;  // the hits come in ascending global id
         for_each_range<D>(L, xj, [&](int b, int e) {
             for (int h = b; h < e; ++h) {
                 double y[3];
@@ -536,7 +574,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
                 for (int q = 0; q < D; ++q) y[q] = L.x[q][h];
                 const double r2 = dist2_nofma<D>(xj, y);
                 if (r2 < d2) {
-                    const int lh = find_sorted(pid, np, h);
+                    const int lh = find_from(pid, np, h, pos);
                     if (lh >= 0) s = fma(wendland<K>(sqrt(r2) * inv), X[lh], s);
                 }
             }

@@ -89,3 +89,32 @@ def test_fuzz_thresholded_against_oracle(msk, ctx, seed):
     for l in range(H.L):
         assert np.linalg.norm(a[l] - ao[l]) <= 1e-9 * np.linalg.norm(ao[l]) + 1e-300, (seed, T, l)
     h.close()
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_fuzz_partitioned_bitwise(msk, ctx, seed):
+    """The partitioned solve (single-GPU emulation, every level with enough
+    chunks partitioned) on random hierarchies: the persistent peer-memory CG
+    (k_pcg) reproduces the single-GPU alpha, iteration counts and s_L bit for
+    bit, for a random world size and both schedules; matrix-free hierarchies
+    take the phase path and must match as well."""
+    H, f, x = _random_hierarchy(200 + seed)
+    rng = np.random.default_rng(seed)
+    world = int(rng.integers(2, 6))
+    flags = msk.MSK_FLAG_MATRIX_FREE if seed % 4 == 3 else 0
+    schedule = "literal" if seed % 2 else "pruned"
+    out = []
+    for c, fl in ((ctx, flags), (msk.Context(0, rank=-1, world=world), flags | msk.MSK_FLAG_DIST_ALL)):
+        h = msk.Hierarchy(c, H.points, H.delta, H.q, k=H.k, flags=fl)
+        h.assemble()
+        a, info = h.solve(f, tol=1e-12, schedule=schedule)
+        s, _ = h.evaluate(x)
+        out.append((a, list(info.cg_iters)[:H.L], s))
+        h.close()
+        if c is not ctx:
+            c.close()
+    (a1, i1, s1), (aw, iw, sw) = out
+    assert iw == i1, (seed, world, iw, i1)
+    for l in range(H.L):
+        assert np.array_equal(aw[l], a1[l]), (seed, world, schedule, l)
+    assert np.array_equal(sw, s1)
