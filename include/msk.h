@@ -209,7 +209,9 @@ MSK_API void msk_hierarchy_destroy(msk_hierarchy *h);
 MSK_API msk_status msk_hierarchy_info_get(const msk_hierarchy *h, msk_hierarchy_info *info);
 
 /* a2 (+ a6): assemble the level matrices A_l in CSR (pattern r^2 <
- * delta_l^2, strict, bit-exact; values Phi_{delta_l}).
+ * delta_l^2, strict, bit-exact; values Phi_{delta_l}).  Any (re-)assembly resets
+ * the solve state (msk_evaluate needs a new msk_solve); a failed one leaves the
+ * hierarchy unassembled (msk_solve => MSK_ERR_STATE).
  *   T <= 0: exact mode; the B_{kl} stay matrix-free and msk_solve runs the
  *           exact Jacobi of Algorithm 2 (inner CG solves).
  *   T > 0:  additionally build the thresholded factor M~(T) (eq:perturbedmatrix

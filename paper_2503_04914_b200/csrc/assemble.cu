@@ -17,7 +17,7 @@ constexpr int NT = 256;
 template <int D>
 __global__ void __launch_bounds__(NT) k_count(LevelView rows, LevelView cols, int same,
                                               int32_t *__restrict__ cnt,
-                                              unsigned long long *__restrict__ min_r2_bits) {
+                                              unsigned long long *__restrict__ min_r2_bits, int64_t row0) {
     int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
     double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     if (i < rows.n) {
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(NT) k_count(LevelView rows, LevelView cols, in
         int c = 0;
         for_each_hit<D>(cols, x, [&](int j, double r2) {
             ++c;
-            if (same && j != i && r2 < best) best = r2;
+            if (same && j != i + row0 && r2 < best) best = r2;  // row0: rows is a slice of cols
         });
         cnt[i] = c;
     }
@@ -128,11 +128,11 @@ void hit_range(int d, const LevelView &rows, const LevelView &cols, unsigned lon
 }
 
 void count_pattern(int d, const LevelView &rows, const LevelView &cols, bool same, int32_t *cnt,
-                   unsigned long long *min_r2_bits, cudaStream_t st, int *launches) {
+                   unsigned long long *min_r2_bits, cudaStream_t st, int *launches, int64_t row0) {
     if (rows.n == 0) return;
     unsigned nb = ceil_div_u(rows.n, NT);
-    if (d == 2) k_count<2><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits);
-    else k_count<3><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits);
+    if (d == 2) k_count<2><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits, row0);
+    else k_count<3><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits, row0);
     MSK_CHECK_LAUNCH();
     if (launches) *launches += 1;
 }

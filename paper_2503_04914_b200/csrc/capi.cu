@@ -130,6 +130,23 @@ int grid_zf() {
     return zf;
 }
 
+// Which levels to partition (DESIGN.md §10): a latency model of one CG
+// iteration.  One GPU moves ~12 nnz + 88 n bytes at ~5 TB/s (measured k_cg:
+// 4.9-5.4 TB/s), with a ~15 us floor (two device barriers and the grid's
+// ramp; C3 levels 1-4 measure 5-15 us); W partitions move 1/W of the bytes
+// each and add the partitioned path's barriers (k_pcg over NVLink: ~10 us
+// per iteration; host-driven phase path with NCCL: ~60 us).  Partition when
+// that is below 0.8 x the one-GPU time.  Identical on every rank (same inputs).
+bool partition_pays(double nnz, double n, int W) {
+    const char *e = getenv("MSK_DIST_P2P");
+    const bool p2p = !(e && e[0] == '0');
+    const double bw = 5e12, floor_s = 15e-6, ovh = p2p ? 10e-6 : 60e-6;
+    const double bytes = 12.0 * nnz + 88.0 * n;
+    const double t1 = std::max(floor_s, bytes / bw);
+    const double tw = std::max(floor_s, bytes / ((double)W * bw)) + ovh;
+    return tw < 0.8 * t1;
+}
+
 // =============================================================== hierarchy
 extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int64_t *n,
                                            const double *const *points, const double *delta,
@@ -240,10 +257,52 @@ extern "C" msk_status msk_hierarchy_create(msk_ctx *ctx, int d, int L, const int
             unsigned long long inf = 0x7ff0000000000000ull;
             MSK_CUDA(cudaMemcpyAsync(minr2[l], &inf, sizeof inf, cudaMemcpyHostToDevice, st));
             LevelView v = h->view(l);
-            count_pattern(d, v, v, true, D.cnt, minr2[l], st, &launches);
+            // distributed context: which levels are partitioned is decided here (the
+            // latency model on an analytic nnz estimate, identical on every rank);
+            // with one GPU per rank a partitioned level counts only its owned rows
+            h->part_on[l] = false;
+            const int W = ctx->world;
+            if (W > 1) {
+                const int64_t rpc = (int64_t)cg_chunk_tiles(n[l]) * 256;
+                const int64_t nch = (n[l] + rpc - 1) / rpc;
+                double vol = 1.0;
+                for (int a = 0; a < d; ++a) vol *= std::max(h->hi[a] - h->lo[a], delta[l]);
+                const double ball = d == 3 ? 4.18879020478639 * delta[l] * delta[l] * delta[l]
+                                           : 3.14159265358979 * delta[l] * delta[l];
+                const double nnz_est = (double)n[l] * std::max(1.0, (double)n[l] * ball / vol);
+                h->part_on[l] = nch >= W && ((flags & MSK_FLAG_DIST_ALL) || partition_pays(nnz_est, (double)n[l], W));
+            }
+            int64_t r0 = 0, r1 = n[l];
+            if (h->part_on[l] && !ctx->emulated) {
+                std::vector<int64_t> b((size_t)W + 1);
+                msk_partition_rows(n[l], W, b.data());
+                r0 = b[ctx->rank];
+                r1 = b[ctx->rank + 1];
+                MSK_CUDA(cudaMemsetAsync(D.cnt, 0, sizeof(int32_t) * (size_t)n[l], st));
+            }
+            LevelView rv = v;
+            rv.n = r1 - r0;
+            for (int a = 0; a < d; ++a) rv.x[a] += r0;
+            count_pattern(d, rv, v, true, D.cnt + r0, minr2[l], st, &launches, r0);
+            D.cnt_lo = r0;
+            D.cnt_hi = r1;
         }
         h->ntot = h->off[L];
         std::vector<unsigned long long> mr(L);
+        // a level whose rows were counted in slices: the minimum over every rank's
+        // slice (each pair is seen by its rows' owners: duplicates are still found)
+        for (int l = 0; l < L; ++l) {
+            if (!(h->part_on[l] && !ctx->emulated)) continue;
+            const int W = ctx->world;
+            unsigned long long *all = dalloc<unsigned long long>((size_t)W, st);
+            MSK_NCCL(nccl_api()->AllGather(minr2[l], all, 1, ncclUint64, ctx->comm, st));
+            std::vector<unsigned long long> hv((size_t)W);
+            MSK_CUDA(cudaMemcpyAsync(hv.data(), all, sizeof(unsigned long long) * W, cudaMemcpyDeviceToHost, st));
+            MSK_CUDA(cudaStreamSynchronize(st));
+            const unsigned long long m = *std::min_element(hv.begin(), hv.end());
+            MSK_CUDA(cudaMemcpyAsync(minr2[l], &m, sizeof m, cudaMemcpyHostToDevice, st));
+            dfree(all, st);
+        }
         for (int l = 0; l < L; ++l)
             MSK_CUDA(cudaMemcpyAsync(&mr[l], minr2[l], sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         tm.stop();
@@ -542,22 +601,7 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
 namespace {
 void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch_R, int64_t patch_min_n, bool mf);
 
-// Which levels to partition (DESIGN.md §10): a latency model of one CG
-// iteration.  One GPU moves ~12 nnz + 88 n bytes at ~5 TB/s (measured k_cg:
-// 4.9-5.4 TB/s), with a ~15 us floor (two device barriers and the grid's
-// ramp; C3 levels 1-4 measure 5-15 us); W partitions move 1/W of the bytes
-// each and add the partitioned path's barriers (k_pcg over NVLink: ~10 us
-// per iteration; host-driven phase path with NCCL: ~60 us).  Partition when
-// that is below 0.8 x the one-GPU time.  Identical on every rank (same inputs).
-bool partition_pays(double nnz, double n, int W) {
-    const char *e = getenv("MSK_DIST_P2P");
-    const bool p2p = !(e && e[0] == '0');
-    const double bw = 5e12, floor_s = 15e-6, ovh = p2p ? 10e-6 : 60e-6;
-    const double bytes = 12.0 * nnz + 88.0 * n;
-    const double t1 = std::max(floor_s, bytes / bw);
-    const double tw = std::max(floor_s, bytes / ((double)W * bw)) + ovh;
-    return tw < 0.8 * t1;
-}
+
 }
 
 extern "C" msk_status msk_assemble_ex(msk_hierarchy *h, double T, double lagrange_tol, double patch_R,
@@ -596,14 +640,30 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
     tm.start();
     int launches = 0;
     std::vector<int64_t> nnz(h->L);
+    // a partitioned level counted only its owned rows at create; the thresholded
+    // factor build needs the full A_l of the column levels: count the others now
+    for (int l = 0; l + 1 < h->L && T > 0.0; ++l) {
+        LevelData &D = h->lev[l];
+        if (D.cnt_lo == 0 && D.cnt_hi == D.n) continue;
+        const LevelView v = h->view(l);
+        for (int part = 0; part < 2; ++part) {
+            const int64_t r0 = part == 0 ? 0 : D.cnt_hi, r1 = part == 0 ? D.cnt_lo : D.n;
+            if (r1 <= r0) continue;
+            LevelView rv = v;
+            rv.n = r1 - r0;
+            for (int a = 0; a < h->d; ++a) rv.x[a] += r0;
+            count_pattern(h->d, rv, v, true, D.cnt + r0, nullptr, st, &launches, r0);
+        }
+        D.cnt_lo = 0;
+        D.cnt_hi = D.n;
+    }
     // distributed context: partition the large levels
     const int W = h->ctx->world;
     for (int l = 0; l < h->L && W > 1; ++l) {
         const int64_t n = h->lev[l].n;
         const int64_t rpc = (int64_t)cg_chunk_tiles(n) * 256;
         const int64_t nch = (n + rpc - 1) / rpc;
-        if (nch >= W && ((h->flags & MSK_FLAG_DIST_ALL) ||
-                         partition_pays((double)sum_i32(h->lev[l].cnt, n, st), (double)n, W))) {
+        if (h->part_on[l]) {  // decided in msk_hierarchy_create (latency model or DIST_ALL)
             auto &Dd = h->dist[l];
             Dd.on = true;
             Dd.rows.resize(W + 1);

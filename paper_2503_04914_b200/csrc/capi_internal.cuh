@@ -53,7 +53,8 @@ struct LevelData {
     double *xs = nullptr;          // d * n SoA, spatial order
     int32_t *perm = nullptr;       // spatial -> caller
     int32_t *cell_start = nullptr; // ncells + 1
-    int32_t *cnt = nullptr;        // A_l row counts (spatial order)
+    int32_t *cnt = nullptr;        // A_l row counts (spatial order), valid on rows [cnt_lo, cnt_hi)
+    int64_t cnt_lo = 0, cnt_hi = 0;
     int64_t nnz = 0;
     int64_t *row_ptr = nullptr;
     int32_t *col = nullptr;
@@ -244,6 +245,7 @@ struct msk_hierarchy {
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     LevelData lev[kMaxLevels];
     bool assembled = false, solved = false;
+    bool part_on[kMaxLevels] = {false};  // distributed context: level partitioned in row blocks
     int64_t ntot = 0;
     int64_t off[kMaxLevels + 1] = {0};
     double *ws = nullptr;  // CG workspace: r, p, q, beta, t (5 * ntot)

@@ -29,7 +29,8 @@ void build_cell_list(int d, int64_t n, const double *pts_rm, const Grid &g, bool
 // Row counts of A_l (or of a rectangular block rows x cols when rows != cols)
 // and the minimum off-diagonal squared distance / duplicate flag.
 void count_pattern(int d, const LevelView &rows, const LevelView &cols, bool same, int32_t *cnt,
-                   unsigned long long *min_r2_bits, cudaStream_t st, int *launches);
+                   unsigned long long *min_r2_bits, cudaStream_t st, int *launches,
+                   int64_t row0 = 0);
 // Fill CSR columns (column spatial index) and values Phi_{delta_col}.
 void fill_pattern(int d, int k, const LevelView &rows, const LevelView &cols,
                   const int64_t *row_ptr, int32_t *col, double *val, cudaStream_t st,
