@@ -59,6 +59,7 @@ extern "C" void msk_ctx_destroy(msk_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    for (auto &M : ctx->peer) M.release();
     if (ctx->comm) nccl_api()->CommDestroy(ctx->comm);
     if (ctx->cin) { cudaStreamSynchronize(ctx->cin); cudaStreamDestroy(ctx->cin); }
     if (ctx->cout) { cudaStreamSynchronize(ctx->cout); cudaStreamDestroy(ctx->cout); }

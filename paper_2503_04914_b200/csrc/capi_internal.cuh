@@ -21,6 +21,30 @@ using namespace msk;
 
 
 // ------------------------------------------------------------------ state
+// Peer-memory buffers for k_pcg on separate GPUs, one set per level index:
+// this rank's r, chunk partials, result and barrier counters (cudaMalloc,
+// exported by IPC handle) and every rank's as mapped in this process.  They
+// live in the CONTEXT and are reused by every hierarchy of the context (grown
+// collectively when a level needs more), so a create/solve/destroy cycle
+// pays no allocation or IPC mapping; the counters keep counting across solves.
+struct PeerMem {
+    bool tried = false, ok = false;
+    int64_t ncap = 0, chcap = 0;  // capacities: rows, chunk partials (3 x chcap)
+    double *r = nullptr, *part = nullptr, *alpha = nullptr;
+    unsigned long long *cnt = nullptr;  // xcnt, nbar, gbar
+    std::vector<double *> pr, ppart, palpha;
+    std::vector<unsigned long long *> pcnt;
+    std::vector<void *> opened;  // IPC-opened peer bases (closed on release)
+    void release() {
+        for (void *p : opened) cudaIpcCloseMemHandle(p);
+        if (r) cudaFree(r);
+        if (part) cudaFree(part);
+        if (alpha) cudaFree(alpha);
+        if (cnt) cudaFree(cnt);
+        *this = PeerMem();
+    }
+};
+
 struct msk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -42,6 +66,7 @@ struct msk_ctx {
         if (!cout) MSK_CUDA(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
         return cout;
     }
+    PeerMem peer[16];  // by level index (kMaxLevels)
 };
 
 namespace capi {
@@ -283,39 +308,18 @@ struct msk_hierarchy {
         double *val = nullptr;
         int64_t hlo = 0, hhi = 0;  // columns referenced by the owned rows: [hlo, hhi)
     };
-    // peer-memory buffers of a partitioned level for k_pcg on separate GPUs:
-    // this rank's r, chunk partials, result and barrier counters (cudaMalloc,
-    // exported by IPC handle), and every rank's as mapped in this process
-    struct PeerMem {
-        bool tried = false, ok = false;
-        double *r = nullptr, *part = nullptr, *alpha = nullptr;
-        unsigned long long *cnt = nullptr;  // xcnt, nbar, gbar
-        std::vector<double *> pr, ppart, palpha;
-        std::vector<unsigned long long *> pcnt;
-        std::vector<void *> opened;  // IPC-opened peer bases (closed on release)
-    };
     struct LevelDist {
         bool on = false;
         std::vector<int64_t> rows;       // world + 1 row bounds
         std::vector<int64_t> hlo, hhi;   // per rank
         std::vector<PartLocal> local;
-        PeerMem peer;
     };
     LevelDist dist[kMaxLevels];
 
     void release_dist() {
         cudaStream_t s = st();
-        bool any_peer = false;
-        for (int l = 0; l < kMaxLevels; ++l) any_peer = any_peer || dist[l].peer.tried;
-        if (any_peer) cudaStreamSynchronize(s);  // no kernel may still use peer memory
         for (int l = 0; l < kMaxLevels; ++l) {
             for (auto &P : dist[l].local) { dfree(P.rp, s); dfree(P.col, s); dfree(P.val, s); }
-            PeerMem &M = dist[l].peer;
-            for (void *p : M.opened) cudaIpcCloseMemHandle(p);
-            if (M.r) cudaFree(M.r);
-            if (M.part) cudaFree(M.part);
-            if (M.alpha) cudaFree(M.alpha);
-            if (M.cnt) cudaFree(M.cnt);
             dist[l] = LevelDist();
         }
     }

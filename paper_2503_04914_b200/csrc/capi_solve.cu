@@ -106,14 +106,22 @@ bool dist_p2p_enabled() {
 // all-gather the IPC handles over NCCL, open the peers'.  Every rank makes the
 // same calls; a failure anywhere (e.g. ranks sharing one device in one process,
 // no peer access) is agreed on by an all-reduce and every rank falls back to
-// the phase path.  Done once per level and assembly (cached in dist[l].peer).
+// the phase path.  Cached in the context per level index and reused by every
+// later hierarchy of the context (grown collectively when a level is larger).
 bool peer_setup(msk_hierarchy *h, int l, int64_t nch) {
-    auto &M = h->dist[l].peer;
-    if (M.tried) return M.ok;
-    M.tried = true;
-    cudaStream_t st = h->st();
-    const int W = h->ctx->world, me = h->ctx->rank;
+    auto &M = h->ctx->peer[l];
     const int64_t n = h->lev[l].n;
+    if (M.tried && !M.ok) return false;              // this context cannot map peers
+    if (M.ok && M.ncap >= n && M.chcap >= nch) return true;  // reuse (every rank decides alike)
+    cudaStream_t st = h->st();
+    if (M.ok) {  // grow: all ranks are here (same n, nch); no kernel may use the old buffers
+        MSK_CUDA(cudaStreamSynchronize(st));
+        M.release();
+    }
+    M.tried = true;
+    M.ncap = n;
+    M.chcap = nch;
+    const int W = h->ctx->world, me = h->ctx->rank;
     int fail = 0;
     auto ck = [&](cudaError_t e) {
         if (e != cudaSuccess) { cudaGetLastError(); fail = 1; }
@@ -472,7 +480,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         const bool p2p = part && !mf && dist_p2p_enabled() && (emu || peer_setup(h, l, nch));
         if (p2p && !emu) {
             // ---- one GPU per rank: this rank's k_pcg over the peers' mapped buffers
-            auto &M = Dd.peer;
+            auto &M = h->ctx->peer[l];
             const auto &P = Dd.local[0];
             PeerCGArgs pa{};
             pa.L = args[0].L;
