@@ -104,22 +104,6 @@ struct __align__(16) CGSharedTT {
     unsigned arr[NSTG];  // asynchronous stage release: warps done with the stage (+8 per use)
 };
 
-// Work buffers of the balanced (segmented) SpMV variant, spmv_phase<..., SEG>:
-// each thread takes 8 consecutive entries of a piece instead of its own rows.
-template <int C>
-struct __align__(16) SegBufT {
-    double rowacc[MAXCH * NT];   // the chunk's row sums (piece contributions in order)
-    double carry[NT];            // a thread's first segment when it continues a row
-    uint16_t rowid[C + 16];      // chunk row of every entry of the piece
-    int16_t crow[NT];            // row of carry[t], -1 if none
-    uint8_t copen[NT];           // that segment also continues past the thread's slice
-};
-template <int C>
-struct __align__(16) CGSharedSeg {
-    CGSharedTT<C> b;
-    SegBufT<C> g;
-};
-
 // ctr == nullptr: the group is one thread-block cluster (small levels, see
 // cg_batched) and the hardware cluster barrier (release / acquire at cluster
 // scope) replaces the counter in global memory.
@@ -238,11 +222,11 @@ __device__ __forceinline__ int col16_decode(uint32_t c, const int4 &b) {
 struct NoPush {
     __device__ __forceinline__ void operator()(int64_t, double) const {}
 };
-template <int C, bool PLAIN = false, class Push = NoPush, bool C16 = false, bool SEG = false>
+template <int C, bool PLAIN = false, class Push = NoPush, bool C16 = false>
 __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &L, int me, int nb, int64_t cbase,
                                            int64_t nloc, int CH, double *part_out, PipeState &ps, uint64_t pol,
                                            bool first, double alpha_prev, double beta,
-                                           const Push &push = Push(), SegBufT<C> *G = nullptr) {
+                                           const Push &push = Push()) {
     // C16: 16-bit columns (L.col16 + per-chunk window bases L.cbase), 10 B per entry
     auto issue = [&](int b, int64_t kb, int64_t ke) {
         if constexpr (C16) issue_piece_16(S, b, L.col16, L.val, kb, ke, pol);
@@ -327,7 +311,6 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             rb[t] = ok ? rp[r] : 0;
             re[t] = ok ? rp[r + 1] : 0;
             acc[t] = 0.0;
-            if constexpr (SEG) G->rowacc[t * NT + tid] = 0.0;
         }
         for (int64_t kb = rp[0]; kb < K1;) {
             const int64_t ke = kb + CAPTE < K1 ? kb + CAPTE : K1;
@@ -354,83 +337,6 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             const CtaStageT<C> &cur = S.st[ps.P & 1];
             const int voff = (int)(kb & 1), coff = C16 ? (int)(kb & 7) : (int)(kb & 3);
             const uint16_t *col16 = reinterpret_cast<const uint16_t *>(cur.col);
-            if constexpr (SEG) {
-                // ---- balanced: (a) every row owner tags its entries of the piece with
-                // the chunk row; (b) thread t sums entries [8t, 8t + 8) as fma chains
-                // per row segment; a segment that continues a row from thread t - 1
-                // goes to carry[t]; (c) the thread holding a row's first segment of
-                // the piece adds the carries that follow it, left to right, into
-                // rowacc.  Row sum = pieces in order, each = its segments left to
-                // right: deterministic (not the row-per-thread chain).
-                const int nE = (int)(ke - kb);
-#pragma unroll
-                for (int t = 0; t < MAXCH; ++t) {
-                    if (t >= CH) break;
-                    const int64_t lo64 = rb[t] > kb ? rb[t] : kb, hi64 = re[t] < ke ? re[t] : ke;
-                    for (int64_t e = lo64; e < hi64; ++e) G->rowid[e - kb] = (uint16_t)(t * NT + tid);
-                }
-                __syncthreads();
-                const int u0 = tid * 8;
-                int hrow = -1;          // row of this thread's last segment if it is a head that stays open
-                double hsum = 0.0;
-                G->crow[tid] = -1;
-                G->copen[tid] = 0;
-                if (u0 < nE) {
-                    const int u1 = u0 + 8 < nE ? u0 + 8 : nE;
-                    double pv[8], vv[8];
-                    int ri[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int u = u0 + j;
-                        const bool ok = u < u1;
-                        const int cj = ok ? (C16 ? col16_decode(col16[coff + u], wb) : cur.col[coff + u]) : 0;
-                        pv[j] = ok ? rv[cj] : 0.0;
-                        vv[j] = ok ? cur.val[voff + u] : 0.0;
-                        ri[j] = ok ? (int)G->rowid[u] : -1;
-                    }
-                    // row of the entry before the slice (same row => continuation)
-                    const int prev = u0 > 0 ? (int)G->rowid[u0 - 1] : -1;
-                    const int next = u1 < nE ? (int)G->rowid[u1] : -1;
-                    double sacc = 0.0;
-                    int r = ri[0];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        if (ri[j] < 0) break;
-                        if (ri[j] != r) {  // segment [.., j) of row r is complete
-                            if (r == prev && G->crow[tid] < 0) {
-                                G->carry[tid] = sacc;
-                                G->crow[tid] = (int16_t)r;
-                            } else {
-                                G->rowacc[r] += sacc;  // a whole row inside the slice (or its head)
-                            }
-                            r = ri[j];
-                            sacc = 0.0;
-                        }
-                        sacc = fma(vv[j], pv[j], sacc);
-                    }
-                    // the last segment (row r)
-                    const bool cont = r == prev && G->crow[tid] < 0;  // also the first segment
-                    const bool open = r == next;
-                    if (cont) {
-                        G->carry[tid] = sacc;
-                        G->crow[tid] = (int16_t)r;
-                        G->copen[tid] = open ? 1 : 0;
-                    } else if (open) {
-                        hrow = r;  // head of a row continuing in the next thread(s)
-                        hsum = sacc;
-                    } else {
-                        G->rowacc[r] += sacc;
-                    }
-                }
-                __syncthreads();
-                if (hrow >= 0) {  // add the continuations, left to right
-                    for (int t2 = tid + 1; t2 < NT && G->crow[t2] == hrow; ++t2) {
-                        hsum += G->carry[t2];
-                        if (!G->copen[t2]) break;
-                    }
-                    G->rowacc[hrow] += hsum;
-                }
-            } else {
 #pragma unroll
             for (int t = 0; t < MAXCH; ++t) {
                 if (t >= CH) break;
@@ -454,7 +360,6 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
                         if (e + u < hi) acc[t] = fma(vv[u], pv[u], acc[t]);
                 }
             }
-            }  // !SEG
             // stage P%NSTG consumed by every thread: it may be refilled.  (Per-warp
             // release through "empty" mbarriers instead was slower: 35.1 vs 33.4 ms.)
             if (ASYNC && kb + 2 * CAPTE < K1) {
@@ -483,11 +388,6 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
             kb = ke;
         }
         double dot = 0.0;
-        if constexpr (SEG) {
-#pragma unroll
-            for (int t = 0; t < MAXCH; ++t)
-                if (t < CH) acc[t] = G->rowacc[t * NT + tid];
-        }
         if (PLAIN) {
 #pragma unroll
             for (int t = 0; t < MAXCH; ++t) {
@@ -540,12 +440,10 @@ __device__ __forceinline__ void spmv_phase(CGSharedTT<C> &S, const CGLevelArgs &
     ps.CS += (uint32_t)K;
 }
 
-template <int C, int MB, bool SEG = false>
+template <int C, int MB>
 __global__ void __launch_bounds__(NT, MB) k_cg(CGBatch B) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CGSharedTT<C> &S = *reinterpret_cast<CGSharedTT<C> *>(smem_raw);
-    // SEG: the balanced SpMV's work buffers follow the pipeline's (CGSharedSeg)
-    SegBufT<C> *G = SEG ? &reinterpret_cast<CGSharedSeg<C> *>(smem_raw)->g : nullptr;
 
     int g = 0;
     while (g + 1 < B.nlev && (int)blockIdx.x >= B.lev[g + 1].block_begin) ++g;
@@ -605,10 +503,7 @@ __global__ void __launch_bounds__(NT, MB) k_cg(CGBatch B) {
             if (it >= L.max_iter) { status = 1; break; }
             tick(-1);
             // ---- w = A r ; p = r + beta p ; q = w + beta q ; x += alpha p_old ; pq = p.q
-            if constexpr (SEG)
-                spmv_phase<C, false, NoPush, false, true>(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol,
-                                                          it == 0, alpha, beta, NoPush(), G);
-            else if (L.col16)
+            if (L.col16)
                 spmv_phase<C, false, NoPush, true>(S, L, me, nb, 0, nchunks, CH, part + nchunks, ps, pol, it == 0,
                                                    alpha, beta);
             else
@@ -1555,7 +1450,7 @@ struct CGVariant {
 // only, and co-residency depends on the device.  Set once per device under a
 // mutex (several host threads -- e.g. the threaded-rank tests -- may race here).
 constexpr int kMaxDevices = 64;
-CGVariant g_var_dev[kMaxDevices][4];
+CGVariant g_var_dev[kMaxDevices][3];
 bool g_var_done[kMaxDevices] = {false};
 std::mutex g_var_mu;
 thread_local CGVariant *g_var = g_var_dev[0];
@@ -1573,12 +1468,9 @@ void set_smem_attrs() {
                 sizeof(CGSharedTT<CAPT1>), 0};
     g_var[2] = {(const void *)k_cg<CAPT2, MINB2>, (const void *)k_dcg_spmv<CAPT2, MINB2>,
                 sizeof(CGSharedTT<CAPT2>), 0};
-    // the balanced (segmented) SpMV variant of the short-row pieces (MSK_SEG=1)
-    g_var[3] = {(const void *)k_cg<CAPT0, 2, true>, (const void *)k_dcg_spmv<CAPT0, MINB0>,
-                sizeof(CGSharedSeg<CAPT0>), 0};
     int sms = 0;
     MSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    for (int vi = 0; vi < 4; ++vi) {
+    for (int vi = 0; vi < 3; ++vi) {
         CGVariant &v = g_var[vi];
         MSK_CUDA(cudaFuncSetAttribute(v.cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
         MSK_CUDA(cudaFuncSetAttribute(v.dcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
@@ -1600,13 +1492,6 @@ void set_smem_attrs() {
     MSK_CUDA(cudaFuncSetAttribute(k_spmv_t<CAPT1, MINB1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(CGSharedTT<CAPT1>)));
     g_var_done[dev] = true;
-}
-
-// MSK_SEG=1: the balanced (segmented) SpMV for the short-row, multi-tile-chunk
-// launches
-bool cg_seg() {
-    static const bool on = getenv("MSK_SEG") && getenv("MSK_SEG")[0] == '1';
-    return on;
 }
 
 // variant by mean row length (entries per row of the work being launched)
@@ -1657,7 +1542,6 @@ void cg_batched(CGLevelArgs *levels, int nlev, cudaStream_t st, int *launches) {
     int vi = 0;
     if (cg_variant(snnz, srows) == 1 || schunks <= g_var[1].resident) vi = 1;
     else if (cg_chunk_tiles(levels[dom].n) == 1) vi = 2;
-    else if (cg_seg()) vi = 3;
     const CGVariant &var = g_var[vi];
     const int total = var.resident;
     if (total < nlev) throw Error(3, "cg_batched: fewer resident CTAs than levels");
