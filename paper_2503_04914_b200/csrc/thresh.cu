@@ -428,19 +428,20 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     const int tid = threadIdx.x;
     const LevelView &L = a.Lv;
     const int pmax = a.pmax;
-    unsigned char *ptr = base;
-    int32_t *pid = reinterpret_cast<int32_t *>(ptr);
-    ptr += sizeof(int32_t) * (size_t)pmax;
-    int32_t *prow = reinterpret_cast<int32_t *>(ptr);
-    ptr += sizeof(int32_t) * (size_t)(pmax + 1);
-    int32_t *pcnt = reinterpret_cast<int32_t *>(ptr);
-    ptr += sizeof(int32_t) * (size_t)pmax;
-    ptr = reinterpret_cast<unsigned char *>(((uintptr_t)ptr + 15) & ~(uintptr_t)15);
-    double *X = reinterpret_cast<double *>(ptr);
+    // byte offsets from base (base is 16-byte aligned; no integer round trip of
+    // the pointers, so a shared-memory base keeps shared addressing)
+    const size_t o_prow = sizeof(int32_t) * (size_t)pmax, o_pcnt = o_prow + sizeof(int32_t) * (size_t)(pmax + 1);
+    const size_t o_x = (o_pcnt + sizeof(int32_t) * (size_t)pmax + 15) & ~(size_t)15;
+    const size_t o_pcol = o_x + sizeof(double) * (4 * (size_t)pmax + (size_t)a.nnzmax);
+    const size_t o_ccnt = (o_pcol + sizeof(uint16_t) * (size_t)a.nnzmax + 15) & ~(size_t)15;
+    int32_t *pid = reinterpret_cast<int32_t *>(base);
+    int32_t *prow = reinterpret_cast<int32_t *>(base + o_prow);
+    int32_t *pcnt = reinterpret_cast<int32_t *>(base + o_pcnt);
+    double *X = reinterpret_cast<double *>(base + o_x);
     double *Rv = X + pmax, *P = Rv + pmax, *Q = P + pmax;
     double *pval = Q + pmax;
-    uint16_t *pcol = reinterpret_cast<uint16_t *>(pval + a.nnzmax);
-    int32_t *ccnt = reinterpret_cast<int32_t *>(((uintptr_t)(pcol + a.nnzmax) + 15) & ~(uintptr_t)15);  // 1024 counters
+    uint16_t *pcol = reinterpret_cast<uint16_t *>(base + o_pcol);
+    int32_t *ccnt = reinterpret_cast<int32_t *>(base + o_ccnt);  // 1024 counters
     double xc[3];
 #pragma unroll
     for (int t = 0; t < D; ++t) xc[t] = L.x[t][i];
@@ -583,10 +584,13 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     }
 }
 
-template <int D, int K>
+// GWS = false: the workspace is the dynamic shared memory, addressed as such
+// (LDS/STS; a pointer that may be either is generic LD/ST with 64-bit
+// addresses); GWS = true: a global slice per CTA for patches that do not fit
+template <int D, int K, bool GWS>
 __global__ void __launch_bounds__(NT) k_patch(PatchArgs a, unsigned char *gws, size_t gstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = gws ? gws + (size_t)blockIdx.x * gstride : smem_raw;
+    unsigned char *base = GWS ? gws + (size_t)blockIdx.x * gstride : smem_raw;
     for (int64_t i = blockIdx.x; i < a.ncols; i += gridDim.x) {
         patch_column<D, K>(a, i, base);
         __syncthreads();  // the workspace is reused by the next column
@@ -612,8 +616,10 @@ void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launc
     MSK_CUDA(cudaGetDevice(&dev));
     MSK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa{};
-    if (a.d == 2) MSK_CUDA(cudaFuncGetAttributes(&fa, a.k == 0 ? k_patch<2, 0> : a.k == 1 ? k_patch<2, 1> : k_patch<2, 2>));
-    else MSK_CUDA(cudaFuncGetAttributes(&fa, a.k == 0 ? k_patch<3, 0> : a.k == 1 ? k_patch<3, 1> : k_patch<3, 2>));
+    if (a.d == 2)
+        MSK_CUDA(cudaFuncGetAttributes(&fa, a.k == 0 ? k_patch<2, 0, false> : a.k == 1 ? k_patch<2, 1, false> : k_patch<2, 2, false>));
+    else
+        MSK_CUDA(cudaFuncGetAttributes(&fa, a.k == 0 ? k_patch<3, 0, false> : a.k == 1 ? k_patch<3, 1, false> : k_patch<3, 2, false>));
     const bool global = smem + fa.sharedSizeBytes > (size_t)optin;
     unsigned grid = (unsigned)a.ncols;
     unsigned char *gws = nullptr;
@@ -625,10 +631,13 @@ void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launc
     const size_t dyn = global ? 0 : smem;
 #define MSK_PT(DD, KK)                                                                            \
     do {                                                                                         \
-        if (!global)                                                                             \
-            MSK_CUDA(cudaFuncSetAttribute(k_patch<DD, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+        if (!global) {                                                                           \
+            MSK_CUDA(cudaFuncSetAttribute(k_patch<DD, KK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                           (int)smem));                                           \
-        k_patch<DD, KK><<<grid, NT, dyn, st>>>(a, gws, stride);                                  \
+            k_patch<DD, KK, false><<<grid, NT, dyn, st>>>(a, gws, stride);                       \
+        } else {                                                                                 \
+            k_patch<DD, KK, true><<<grid, NT, dyn, st>>>(a, gws, stride);                        \
+        }                                                                                        \
     } while (0)
     if (a.d == 2) {
         if (a.k == 0) MSK_PT(2, 0); else if (a.k == 1) MSK_PT(2, 1); else MSK_PT(2, 2);
