@@ -511,7 +511,13 @@ void build_factor(msk_hierarchy *h, double T, double lagrange_tol, double patch_
             // the members' row lengths bound the patch-local entries (the workspace, and
             // with it the CTAs per SM, is sized by it instead of pmax x max row length)
             pa.nnzmax = (int)std::min<int64_t>((int64_t)hpz[1], (int64_t)hp * hp);
-            const size_t smem = patch_smem_bytes(pa.pmax, pa.nnzmax);
+            {
+                const int64_t side = 2 * (int64_t)pa.reach + 1, nq = d == 3 ? side * side : side;
+                if (nq > 65535)
+                    throw Error(MSK_ERR_INVALID, "msk_assemble: local patch spans too many cells; reduce patch_R");
+                pa.nq = (int)nq;
+            }
+            const size_t smem = patch_smem_bytes(pa.pmax, pa.nnzmax, pa.nq);
             // larger patches run from a global workspace (patch_lagrange); bound it
             if (smem > (size_t)1 << 30)
                 throw Error(MSK_ERR_INVALID, "msk_assemble: local patch too large (" + std::to_string(hp) +

@@ -318,6 +318,7 @@ struct PatchArgs {
     double rho2;                    // patch radius^2 (no-FMA test, reading C-4 recipe)
     int reach;                      // cells of level l's grid spanned by rho
     int pmax, nnzmax;               // shared-memory capacity (points, local entries)
+    int nq;                         // patch columns of the box, (2 reach + 1)^(d-1)
     LevelView Lv;                   // the coarse level (cells, SoA coordinates)
     const int64_t *row_ptr;         // A_l (spatial)
     const int32_t *col;
@@ -339,7 +340,7 @@ struct PatchArgs {
 // sum of the members' row lengths of A_l (rowcnt; bounds the patch-local entries) into [1]
 void patch_count(const PatchArgs &a, const int32_t *rowcnt, int *pmax_out, cudaStream_t st);
 void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launches);
-size_t patch_smem_bytes(int pmax, int nnzmax);
+size_t patch_smem_bytes(int pmax, int nnzmax, int nq);
 // out[g] = base[g] - sum_p val[p] v[col[p]] for global rows g in [r0, r1)
 // bucket/tmax (optional): only entries with bucket <= tmax take part (the T sweep)
 void csc_spmv_add(int64_t ncols, const int64_t *cptr, const int64_t *cpos, const int32_t *crow, const double *val,

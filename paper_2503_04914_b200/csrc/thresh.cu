@@ -258,26 +258,34 @@ __global__ void __launch_bounds__(NT) k_csc_spmv_add(int64_t ncols, const int64_
 //
 // A CTA owns coarse column i of level l:
 //  1. patch P = level-l points with |x_h - x_i|^2 < rho^2, enumerated over the
-//     (2m+1)^(d-1) z-columns of cells around x_i in increasing key order, so the
-//     global ids pid[] come out ascending (count, block scan, write);
-//  2. local CSR of A_P: rows of A_l restricted to columns in P (binary search
-//     in pid[]), values copied (count, block scan, fill);
+//     nq <= (2m+1)^(d-1) z-columns of cells around x_i in increasing key order
+//     (the "patch columns" of the box), so the global ids pid[] come out
+//     ascending; per patch column its id range [cb, ce) and member range
+//     [ccnt[q], ccnt[q+1]) are kept, per member its column pq[];
+//  2. local CSR of A_P: row r of A_l restricted to the members.  A_l's
+//     neighbours of a point lie in the 3^(d-1) columns around its own, which
+//     are visited in ascending order with a monotone member pointer each (no
+//     search); values copied;
 //  3. CG on A_P c = e_i (x0 = 0, stop ||r|| <= lagrange_tol, reading C-9),
-//     vectors in shared memory, block_sum reductions (deterministic);
+//     vectors in shared memory, in the single-reduction form of k_cg (q = A r
+//     + beta q by recurrence: one fixed-order block reduction of r.r and r.Ar
+//     per iteration);
 //  4. for each stored entry (fine point x_j) of column i:
 //     chi~_i(x_j) = delta_l^-d sum_{h in P, r < delta_l} phi(r/delta_l) c_h,
-//     h ascending (the order of k_tvalues).
-size_t patch_smem_bytes_impl(int pmax, int nnzmax) {
+//     h ascending (the order of k_tvalues), visiting only the members in the
+//     3^(d-1) patch columns and z window around x_j.
+size_t patch_smem_bytes_impl(int pmax, int nnzmax, int nq) {
     size_t b = 0;
     b += sizeof(int32_t) * (size_t)pmax;          // pid
     b += sizeof(int32_t) * (size_t)(pmax + 1);    // prow (row slots: starts)
     b += sizeof(int32_t) * (size_t)pmax;          // pcnt (entries per row slot)
+    b += sizeof(uint16_t) * (size_t)pmax;         // pq (patch column of each member)
     b = (b + 15) & ~(size_t)15;
-    b += sizeof(double) * 4 * (size_t)pmax;       // x r p q
+    b += sizeof(double) * 5 * (size_t)pmax;       // x r p s w
     b += sizeof(double) * (size_t)nnzmax;         // pval
     b += sizeof(uint16_t) * (size_t)nnzmax;       // pcol (patch-local, < 65536 points)
     b = (b + 15) & ~(size_t)15;
-    b += sizeof(int32_t) * 1024;                  // column counts / scan scratch
+    b += sizeof(int32_t) * (3 * (size_t)nq + 1);  // ccnt (member starts), cb, ce (id ranges)
     return b + 64;
 }
 
@@ -341,34 +349,6 @@ __global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, const int32_t *
     atomicMax(pmax_out + 1, (int)(nz < 0x7fffffffll ? nz : 0x7fffffffll));
 }
 
-// find_sorted for ascending keys: `pos` is the lower bound of the previous key;
-// a few linear steps from it (a row's columns, or a stored row's hits, come in
-// clusters of nearby global ids), else a binary search of the rest.  Returns
-// the index or -1 and leaves pos at key's lower bound.
-__device__ __forceinline__ int find_from(const int32_t *v, int n, int32_t key, int &pos) {
-    int lo = pos;
-    for (int s = 0; s < 4 && lo < n && v[lo] < key; ++s) ++lo;
-    if (lo < n && v[lo] < key) {
-        int hi = n;
-        ++lo;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (v[mid] < key) lo = mid + 1; else hi = mid;
-        }
-    }
-    pos = lo;
-    return lo < n && v[lo] == key ? lo : -1;
-}
-
-__device__ __forceinline__ int find_sorted(const int32_t *v, int n, int32_t key) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (v[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    return lo < n && v[lo] == key ? lo : -1;
-}
-
 // exclusive block scan of cnt[0..n) in shared memory (n <= NT * k), result in place; returns the total
 __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp /* NT */) {
     const int tid = threadIdx.x;
@@ -404,52 +384,41 @@ __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp
     return total;
 }
 
-// Block sum with ONE barrier (the patch CG is barrier-latency bound: one CTA,
-// ~60 iterations of ~730 rows): warp xor-trees, the warp partials in `buf`,
-// every thread adds them in warp order (a fixed order: deterministic).  The
-// caller alternates two buffers, so a buffer is rewritten only after a later
-// barrier has retired its readers.
-__device__ __forceinline__ double block_sum_1bar(double v, double *buf) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) t += buf[w];
-    return t;
-}
-
 // one column; `base` = the CTA's workspace (shared memory, or a global slice
 // for patches that do not fit); every early return is CTA-uniform
 template <int D, int K>
 __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsigned char *base) {
-    __shared__ double red1[NT / 32], red2[NT / 32];  // the two CG reductions alternate buffers
+    __shared__ double red[2 * (NT / 32)];  // r.r and r.Ar warp partials
     __shared__ int32_t tmp[NT + 1];
     const int tid = threadIdx.x;
     const LevelView &L = a.Lv;
-    const int pmax = a.pmax;
+    const int pmax = a.pmax, nq = a.nq;
     // byte offsets from base (base is 16-byte aligned; no integer round trip of
     // the pointers, so a shared-memory base keeps shared addressing)
     const size_t o_prow = sizeof(int32_t) * (size_t)pmax, o_pcnt = o_prow + sizeof(int32_t) * (size_t)(pmax + 1);
-    const size_t o_x = (o_pcnt + sizeof(int32_t) * (size_t)pmax + 15) & ~(size_t)15;
-    const size_t o_pcol = o_x + sizeof(double) * (4 * (size_t)pmax + (size_t)a.nnzmax);
+    const size_t o_pq = o_pcnt + sizeof(int32_t) * (size_t)pmax;
+    const size_t o_x = (o_pq + sizeof(uint16_t) * (size_t)pmax + 15) & ~(size_t)15;
+    const size_t o_pcol = o_x + sizeof(double) * (5 * (size_t)pmax + (size_t)a.nnzmax);
     const size_t o_ccnt = (o_pcol + sizeof(uint16_t) * (size_t)a.nnzmax + 15) & ~(size_t)15;
     int32_t *pid = reinterpret_cast<int32_t *>(base);
     int32_t *prow = reinterpret_cast<int32_t *>(base + o_prow);
     int32_t *pcnt = reinterpret_cast<int32_t *>(base + o_pcnt);
+    uint16_t *pq = reinterpret_cast<uint16_t *>(base + o_pq);
     double *X = reinterpret_cast<double *>(base + o_x);
-    double *Rv = X + pmax, *P = Rv + pmax, *Q = P + pmax;
-    double *pval = Q + pmax;
+    double *Rv = X + pmax, *P = Rv + pmax, *S = P + pmax, *W = S + pmax;
+    double *pval = W + pmax;
     uint16_t *pcol = reinterpret_cast<uint16_t *>(base + o_pcol);
-    int32_t *ccnt = reinterpret_cast<int32_t *>(base + o_ccnt);  // 1024 counters
+    int32_t *ccnt = reinterpret_cast<int32_t *>(base + o_ccnt);  // nq + 1 member starts
+    int32_t *cb = ccnt + nq + 1, *ce = cb + nq;                   // per patch column: global id range
     double xc[3];
 #pragma unroll
     for (int t = 0; t < D; ++t) xc[t] = L.x[t][i];
     // ---- 1. patch points, ascending global id
     int64_t c[3], x0, x1, y0, y1, z0, z1;
     patch_columns<D>(L, xc, a.reach, c, x0, x1, y0, y1, z0, z1);
-    const int ncolz = (int)((x1 - x0 + 1) * (y1 - y0 + 1));
-    if (ncolz > 1024) {
+    const int nyb = (int)(y1 - y0 + 1);  // 1 in 2-D
+    const int ncolz = (int)((x1 - x0 + 1) * nyb);
+    if (ncolz > nq) {
         if (tid == 0) atomicAdd(&a.fail[1], 1);
         return;
     }
@@ -463,6 +432,8 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
             if (dist2_nofma<D>(xc, y) < a.rho2) ++n;
         }
         ccnt[q] = n;
+        cb[q] = b;
+        ce[q] = e;
     }
     __syncthreads();
     const int np = block_scan_excl(ccnt, ncolz, tmp);
@@ -470,14 +441,19 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         if (tid == 0) atomicAdd(&a.fail[1], 1);
         return;
     }
+    if (tid == 0) ccnt[ncolz] = np;
     for (int q = tid; q < ncolz; q += NT) {
-        int b, e, w = ccnt[q];
-        patch_range<D>(L, q, x0, y0, y1, z0, z1, b, e);
+        int w = ccnt[q];
+        const int b = cb[q], e = ce[q];
         for (int h = b; h < e; ++h) {
             double y[3];
 #pragma unroll
             for (int t = 0; t < D; ++t) y[t] = L.x[t][h];
-            if (dist2_nofma<D>(xc, y) < a.rho2) pid[w++] = h;
+            if (dist2_nofma<D>(xc, y) < a.rho2) {
+                pid[w] = h;
+                pq[w] = (uint16_t)q;
+                ++w;
+            }
         }
     }
     __syncthreads();
@@ -499,58 +475,102 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         if (tid == 0) atomicAdd(&a.fail[1], 1);
         return;
     }
+    constexpr int NS = D == 3 ? 9 : 3;  // neighbour columns (dx, dy) in ascending key order
     for (int r = tid; r < np; r += NT) {
         const int32_t g = pid[r];
-        int w = prow[r], pos = 0;
-        for (int64_t k = a.row_ptr[g]; k < a.row_ptr[g + 1]; ++k) {  // ascending columns
-            const int lc = find_from(pid, np, a.col[k], pos);
-            if (lc >= 0) {
-                pcol[w] = (uint16_t)lc;
+        const int q = pq[r], qx = q / nyb, qy = q - qx * nyb;
+        int w = prow[r];
+        int s = -1, m = 0, mend = 0;
+        int32_t lo = 0, hi = 0;  // the current column's id range
+        auto next = [&]() {
+            while (++s < NS) {
+                const int ax = qx + s / (NS / 3) - 1, ay = D == 3 ? qy + s % 3 - 1 : 0;
+                if (ax < 0 || ax > (int)(x1 - x0) || ay < 0 || ay >= nyb) continue;
+                const int cq = ax * nyb + ay;
+                m = ccnt[cq];
+                mend = ccnt[cq + 1];
+                lo = cb[cq];
+                hi = ce[cq];
+                return true;
+            }
+            return false;
+        };
+        bool have = next();
+        for (int64_t k = a.row_ptr[g]; have && k < a.row_ptr[g + 1]; ++k) {  // ascending columns
+            const int32_t cc = a.col[k];
+            while (have && cc >= hi) have = next();
+            if (!have || cc < lo) continue;
+            while (m < mend && pid[m] < cc) ++m;
+            if (m < mend && pid[m] == cc) {
+                pcol[w] = (uint16_t)m;
                 pval[w] = a.val[k];
                 ++w;
             }
         }
         pcnt[r] = w - prow[r];
     }
-    // ---- 3. CG on A_P c = e_center
-    const int ctr = find_sorted(pid, np, (int32_t)i);
+    // ---- 3. CG on A_P c = e_center, single-reduction form (as k_cg): per
+    // iteration w = A r, then r.r and r.w in ONE block reduction, then
+    // p = r + beta p, s = w + beta s (= A p), x += alpha p, r -= alpha s
+    int ctr = -1;
+    {
+        const int q = (int)((c[0] - x0) * nyb + (D == 3 ? c[1] - y0 : 0));  // the centre's own column
+        for (int m = ccnt[q]; m < ccnt[q + 1]; ++m)
+            if (pid[m] == (int32_t)i) ctr = m;
+    }
     __syncthreads();
     for (int r = tid; r < np; r += NT) {
-        const double e = r == ctr ? 1.0 : 0.0;
         X[r] = 0.0;
-        Rv[r] = e;
-        P[r] = e;
+        Rv[r] = r == ctr ? 1.0 : 0.0;
+        P[r] = 0.0;
+        S[r] = 0.0;
     }
-    double rr = 1.0;
+    double rr_prev = 1.0, alpha = 0.0;
     int it = 0;
     __syncthreads();
-    while (rr > a.tol2) {
+    for (;;) {
+        double vrr = 0.0, vrw = 0.0;
+        for (int r = tid; r < np; r += NT) {
+            double acc = 0.0;
+            const int k0 = prow[r], k1 = k0 + pcnt[r];
+            for (int k = k0; k < k1; ++k) acc = fma(pval[k], Rv[pcol[k]], acc);
+            W[r] = acc;
+            const double rv = Rv[r];
+            vrr += rv * rv;
+            vrw += rv * acc;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            vrr += __shfl_xor_sync(0xffffffffu, vrr, o);
+            vrw += __shfl_xor_sync(0xffffffffu, vrw, o);
+        }
+        if ((tid & 31) == 0) {
+            red[tid >> 5] = vrr;
+            red[NT / 32 + (tid >> 5)] = vrw;
+        }
+        __syncthreads();
+        double rr = 0.0, rw = 0.0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {  // warp order: deterministic
+            rr += red[w];
+            rw += red[NT / 32 + w];
+        }
+        if (rr <= a.tol2) break;
         if (it >= a.max_iter) {
             if (tid == 0) atomicAdd(&a.fail[0], 1);
             break;
         }
-        double pq = 0.0;
+        const double beta = it == 0 ? 0.0 : rr / rr_prev;
+        alpha = it == 0 ? rr / rw : rr / (rw - beta * rr / alpha);
+        rr_prev = rr;
         for (int r = tid; r < np; r += NT) {
-            double acc = 0.0;
-            const int k0 = prow[r], k1 = k0 + pcnt[r];
-            for (int k = k0; k < k1; ++k) acc = fma(pval[k], P[pcol[k]], acc);
-            Q[r] = acc;
-            pq += P[r] * acc;
+            const double pn = Rv[r] + beta * P[r];
+            const double sn = W[r] + beta * S[r];
+            P[r] = pn;
+            S[r] = sn;
+            X[r] += alpha * pn;
+            Rv[r] -= alpha * sn;
         }
-        pq = block_sum_1bar(pq, red1);
-        const double alpha = rr / pq;
-        double rn = 0.0;
-        for (int r = tid; r < np; r += NT) {
-            const double v = Rv[r] - alpha * Q[r];
-            Rv[r] = v;
-            rn += v * v;
-            X[r] += alpha * P[r];
-        }
-        rn = block_sum_1bar(rn, red2);
-        const double beta = rn / rr;
-        rr = rn;
-        for (int r = tid; r < np; r += NT) P[r] = Rv[r] + beta * P[r];
-        __syncthreads();
+        __syncthreads();  // r complete before the next w = A r; red[] read before it is rewritten
         ++it;
     }
     if (tid == 0) atomicMax(&a.fail[2], it);
@@ -558,6 +578,8 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     // ---- 4. values at the stored entries of column i
     const int64_t gc = a.col_off + i;
     const double d2 = L.delta2, inv = L.inv_delta;
+    const int la = D - 1;
+    const int64_t zf = L.g.zf;
     for (int64_t t = a.cptr[gc] + tid; t < a.cptr[gc + 1]; t += NT) {
         const int64_t g = a.crow[t];
         int k = 0;
@@ -566,20 +588,33 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         double xj[3];
 #pragma unroll
         for (int q = 0; q < D; ++q) xj[q] = a.lev_xs[k][(int64_t)q * a.lev_n[k] + j];
-        double s = 0.0;
-        int pos = 0;  // the hits come in ascending global id
-        for_each_range<D>(L, xj, [&](int b, int e) {
-            for (int h = b; h < e; ++h) {
-                double y[3];
+        int64_t cj[3];
 #pragma unroll
-                for (int q = 0; q < D; ++q) y[q] = L.x[q][h];
-                const double r2 = dist2_nofma<D>(xj, y);
-                if (r2 < d2) {
-                    const int lh = find_from(pid, np, h, pos);
-                    if (lh >= 0) s = fma(wendland<K>(sqrt(r2) * inv), X[lh], s);
+        for (int q = 0; q < D; ++q) cj[q] = cell_coord(L.g, q, xj[q]);
+        const int64_t zlo = cj[la] - zf > z0 ? cj[la] - zf : z0, zhi = cj[la] + zf < z1 ? cj[la] + zf : z1;
+        double s = 0.0;
+        if (zlo <= zhi) {
+            for (int64_t ix = cj[0] - 1; ix <= cj[0] + 1; ++ix) {
+                if (ix < x0 || ix > x1) continue;
+                for (int64_t iy = D == 3 ? cj[1] - 1 : 0; iy <= (D == 3 ? cj[1] + 1 : 0); ++iy) {
+                    if (D == 3 && (iy < y0 || iy > y1)) continue;
+                    const int q = (int)((ix - x0) * nyb + (iy - y0));
+                    const int64_t kb = D == 3 ? (ix * L.g.dim[1] + iy) * L.g.dim[2] : ix * L.g.dim[1];
+                    const int32_t b = L.cell_start[kb + zlo], e = L.cell_start[kb + zhi + 1];
+                    // the members in cells zlo..zhi of this column, ascending
+                    for (int m = ccnt[q]; m < ccnt[q + 1]; ++m) {
+                        const int32_t h = pid[m];
+                        if (h < b) continue;
+                        if (h >= e) break;
+                        double y[3];
+#pragma unroll
+                        for (int u = 0; u < D; ++u) y[u] = L.x[u][h];
+                        const double r2 = dist2_nofma<D>(xj, y);
+                        if (r2 < d2) s = fma(wendland<K>(sqrt(r2) * inv), X[m], s);
+                    }
                 }
             }
-        });
+        }
         a.val_out[a.cpos[t]] = L.scale * s;
     }
 }
@@ -598,7 +633,7 @@ __global__ void __launch_bounds__(NT) k_patch(PatchArgs a, unsigned char *gws, s
 }
 }  // namespace
 
-size_t patch_smem_bytes(int pmax, int nnzmax) { return patch_smem_bytes_impl(pmax, nnzmax); }
+size_t patch_smem_bytes(int pmax, int nnzmax, int nq) { return patch_smem_bytes_impl(pmax, nnzmax, nq); }
 
 void patch_count(const PatchArgs &a, const int32_t *rowcnt, int *pmax_out, cudaStream_t st) {
     if (a.ncols <= 0) return;
