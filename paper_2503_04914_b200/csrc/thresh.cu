@@ -282,8 +282,8 @@ size_t patch_smem_bytes_impl(int pmax, int nnzmax, int nq) {
     b += sizeof(uint16_t) * (size_t)pmax;         // pq (patch column of each member)
     b = (b + 15) & ~(size_t)15;
     b += sizeof(double) * 5 * (size_t)pmax;       // x r p s w
-    b += sizeof(double) * (size_t)nnzmax;         // pval
-    b += sizeof(uint16_t) * (size_t)nnzmax;       // pcol (patch-local, < 65536 points)
+    b += sizeof(double) * ((size_t)nnzmax + 1);   // pval (+ a zero sentinel)
+    b += sizeof(uint16_t) * ((size_t)nnzmax + 1); // pcol (patch-local, < 65536 points)
     b = (b + 15) & ~(size_t)15;
     b += sizeof(int32_t) * (3 * (size_t)nq + 1);  // ccnt (member starts), cb, ce (id ranges)
     return b + 64;
@@ -398,8 +398,8 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     const size_t o_prow = sizeof(int32_t) * (size_t)pmax, o_pcnt = o_prow + sizeof(int32_t) * (size_t)(pmax + 1);
     const size_t o_pq = o_pcnt + sizeof(int32_t) * (size_t)pmax;
     const size_t o_x = (o_pq + sizeof(uint16_t) * (size_t)pmax + 15) & ~(size_t)15;
-    const size_t o_pcol = o_x + sizeof(double) * (5 * (size_t)pmax + (size_t)a.nnzmax);
-    const size_t o_ccnt = (o_pcol + sizeof(uint16_t) * (size_t)a.nnzmax + 15) & ~(size_t)15;
+    const size_t o_pcol = o_x + sizeof(double) * (5 * (size_t)pmax + (size_t)a.nnzmax + 1);
+    const size_t o_ccnt = (o_pcol + sizeof(uint16_t) * ((size_t)a.nnzmax + 1) + 15) & ~(size_t)15;
     int32_t *pid = reinterpret_cast<int32_t *>(base);
     int32_t *prow = reinterpret_cast<int32_t *>(base + o_prow);
     int32_t *pcnt = reinterpret_cast<int32_t *>(base + o_pcnt);
@@ -475,6 +475,11 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         if (tid == 0) atomicAdd(&a.fail[1], 1);
         return;
     }
+    const int nnz_sent = a.nnzmax;  // zero entry read by finished rows in the CG's SpMV
+    if (tid == 0) {
+        pval[nnz_sent] = 0.0;
+        pcol[nnz_sent] = 0;
+    }
     constexpr int NS = D == 3 ? 9 : 3;  // neighbour columns (dx, dy) in ascending key order
     for (int r = tid; r < np; r += NT) {
         const int32_t g = pid[r];
@@ -530,14 +535,37 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     __syncthreads();
     for (;;) {
         double vrr = 0.0, vrw = 0.0;
-        for (int r = tid; r < np; r += NT) {
-            double acc = 0.0;
-            const int k0 = prow[r], k1 = k0 + pcnt[r];
-            for (int k = k0; k < k1; ++k) acc = fma(pval[k], Rv[pcol[k]], acc);
-            W[r] = acc;
-            const double rv = Rv[r];
-            vrr += rv * rv;
-            vrw += rv * acc;
+        // a thread's rows rb, rb + NT, rb + 2 NT as three independent chains
+        // (the loads of all three in flight; each row still sums in ascending
+        // k); a finished row reads the zero sentinel entry at nnzmax
+        for (int rb = tid; rb < np; rb += 3 * NT) {
+            int kk[3], ke[3];
+            double acc[3] = {0.0, 0.0, 0.0};
+            int n = 0;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int r = rb + u * NT;
+                kk[u] = r < np ? prow[r] : 0;
+                ke[u] = r < np ? kk[u] + pcnt[r] : 0;
+                n = max(n, ke[u] - kk[u]);
+            }
+            for (int t = 0; t < n; ++t) {
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int k = kk[u] + t < ke[u] ? kk[u] + t : nnz_sent;
+                    acc[u] = fma(pval[k], Rv[pcol[k]], acc[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int r = rb + u * NT;
+                if (r < np) {
+                    W[r] = acc[u];
+                    const double rv = Rv[r];
+                    vrr += rv * rv;
+                    vrw += rv * acc[u];
+                }
+            }
         }
         for (int o = 16; o > 0; o >>= 1) {
             vrr += __shfl_xor_sync(0xffffffffu, vrr, o);
