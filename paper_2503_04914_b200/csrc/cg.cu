@@ -63,6 +63,18 @@ constexpr int NW = NT / 32;   // warps per CTA
 #ifndef MSK_MINB
 #define MSK_MINB 3
 #endif
+#ifndef MSK_MF_U2
+#define MSK_MF_U2 4  // matrix-free SpMV: survivors per trip, 2-D (C2 finest 68.4 -> 54.5 ms)
+#endif
+#ifndef MSK_MF_U3
+#define MSK_MF_U3 2  // 3-D (C3 finest 166 -> 144 ms; 4: 149 ms)
+#endif
+#ifndef MSK_MF_P
+#define MSK_MF_P 4   // candidates per trip of the prefilter (4: C2 finest 54.6 -> 52.2 ms, C3 144 -> 138)
+#endif
+#ifndef MSK_MF_MINB
+#define MSK_MF_MINB 4
+#endif
 #ifndef MSK_ASYNC_MIN_C
 #define MSK_ASYNC_MIN_C 4096
 #endif
@@ -1222,7 +1234,7 @@ __global__ void __launch_bounds__(NT) k_dcg_xfin(DistCGArgs A) {
 // Candidates: conservative FP32 prefilter (gather.cu), then the exact no-FMA
 // test (reading C-4) on the survivors.
 template <int D, int K>
-__global__ void __launch_bounds__(NT, 4) k_mf_spmv(DistCGArgs A, LevelView V) {
+__global__ void __launch_bounds__(NT, MSK_MF_MINB) k_mf_spmv(DistCGArgs A, LevelView V) {
     if (!A.sc->active) return;
     __shared__ double red[NT / 32 + 2];
     constexpr int HM = 40;
@@ -1251,7 +1263,31 @@ __global__ void __launch_bounds__(NT, 4) k_mf_spmv(DistCGArgs A, LevelView V) {
             int hl[HM];
             int nh = 0;
             auto flush = [&]() {
-                for (int h = 0; h < nh; ++h) {
+                int h = 0;
+                // MFU survivors per trip: their records and gathered r values are
+                // loaded up front (independent loads in flight), then accumulated in
+                // ascending order as before (a miss adds nothing: bit-identical)
+                constexpr int MFU = D == 2 ? MSK_MF_U2 : MSK_MF_U3;
+                for (; MFU > 1 && h + MFU <= nh; h += MFU) {
+                    double4 R[MFU];
+                    double rj[MFU];
+#pragma unroll
+                    for (int u = 0; u < MFU; ++u) {
+                        const int j = hl[h + u];
+                        R[u] = rec[j];
+                        rj[u] = rv[j];
+                    }
+#pragma unroll
+                    for (int u = 0; u < MFU; ++u) {
+                        const double y[3] = {R[u].x, R[u].y, R[u].z};
+                        const double r2 = dist2_nofma<D>(x, y);
+                        if (r2 < d2) {
+                            const double v = scl * wendland<K>(sqrt(r2) * inv);
+                            acc = fma(v, rj[u], acc);
+                        }
+                    }
+                }
+                for (; h < nh; ++h) {
                     const int j = hl[h];
                     const double4 R = rec[j];  // packed coordinates (the .w slot is unused here)
                     const double y[3] = {R.x, R.y, R.z};
@@ -1265,6 +1301,24 @@ __global__ void __launch_bounds__(NT, 4) k_mf_spmv(DistCGArgs A, LevelView V) {
             };
             for_each_range<D>(V, x, [&](int b, int e) {
                 int j = b;
+#if MSK_MF_P == 4
+                for (; j + 3 < e; j += 4) {  // four candidates per trip (independent loads)
+                    const float4 F0 = frec[j], F1 = frec[j + 1], F2 = frec[j + 2], F3 = frec[j + 3];
+                    const float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
+                    const float a1 = xf[0] - F1.x, b1 = xf[1] - F1.y, c1 = xf[2] - F1.z;
+                    const float a2 = xf[0] - F2.x, b2 = xf[1] - F2.y, c2 = xf[2] - F2.z;
+                    const float a3 = xf[0] - F3.x, b3 = xf[1] - F3.y, c3 = xf[2] - F3.z;
+                    const bool h0 = fmaf(c0, c0, fmaf(b0, b0, a0 * a0)) < fthr;
+                    const bool h1 = fmaf(c1, c1, fmaf(b1, b1, a1 * a1)) < fthr;
+                    const bool h2 = fmaf(c2, c2, fmaf(b2, b2, a2 * a2)) < fthr;
+                    const bool h3 = fmaf(c3, c3, fmaf(b3, b3, a3 * a3)) < fthr;
+                    if (nh + 4 > HM) flush();
+                    if (h0) hl[nh++] = j;
+                    if (h1) hl[nh++] = j + 1;
+                    if (h2) hl[nh++] = j + 2;
+                    if (h3) hl[nh++] = j + 3;
+                }
+#endif
                 for (; j + 1 < e; j += 2) {  // two candidates per trip (independent loads)
                     const float4 F0 = frec[j], F1 = frec[j + 1];
                     const float a0 = xf[0] - F0.x, b0 = xf[1] - F0.y, c0 = xf[2] - F0.z;
@@ -1791,7 +1845,7 @@ void dcg_mf_spmv(const DistCGArgs &a, const LevelView &v, int d, int k, cudaStre
     const bool v1 = gather_v1();
 #define MSK_MF(DD, KK)                                                                   \
     do {                                                                                 \
-        if (v1) k_mf_spmv<DD, KK><<<dcg_grid(a, 4), NT, 0, st>>>(a, v);                  \
+        if (v1) k_mf_spmv<DD, KK><<<dcg_grid(a, MSK_MF_MINB), NT, 0, st>>>(a, v);                  \
         else k_mf_spmv_w<DD, KK><<<dcg_grid(a, 3), NT, 0, st>>>(a, v);                   \
     } while (0)
     if (d == 2) {
