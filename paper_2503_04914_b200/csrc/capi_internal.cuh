@@ -233,7 +233,9 @@ struct Ev {
     void wait_on(cudaStream_t s) { MSK_CUDA(cudaStreamWaitEvent(s, e, 0)); }
 };
 
-#define API_BEGIN try {
+#define API_BEGIN                          \
+    ::msk::NvtxRange msk_nvtx_api_(__func__); \
+    try {
 #define API_END                                                  \
     return MSK_OK;                                               \
     }                                                            \

@@ -299,6 +299,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         ga.out = out_spatial;
         ga.out_perm = nullptr;
         ga.hits = d_hits;
+        NvtxRange nv("B products");
         time_ga();
         gather(ga, st, &launches);
         ga_t.back()->stop();
@@ -721,6 +722,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
         // alpha^(l) = t^(l) (the final block CG of a converged block is the
         // same solve); the finest level is solved at tol.
         for (int l = 0; l < L; ++l) {
+            NvtxRange nvl("level " + std::to_string(l));
             const double tl = l + 1 < L ? inner_tol : tol;
             wait_f(l);
             if (h->dist[l].on || mf) {
@@ -742,6 +744,7 @@ extern "C" msk_status msk_solve(msk_hierarchy *h, const double *const *f, double
                 set_coef(a, l);
             }
             debug_sync(st, "b_products");
+            NvtxRange nvc("CG");
             time_cg(l);
             cg_batched(&a, 1, st, &launches);
             cg_t.back()->stop();
@@ -925,6 +928,7 @@ void evaluate_pipelined(msk_hierarchy *h, int64_t m, const double *x, double *s,
         ein[c].record(cin);
     }
     for (int64_t c = 0; c < nc; ++c) {
+        NvtxRange nvc("evaluate chunk " + std::to_string(c));
         const int64_t c0 = bnd[c], c1 = bnd[c + 1], nck = c1 - c0;
         ein[c].wait_on(st);
         CellListOut co{};

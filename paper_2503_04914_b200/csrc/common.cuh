@@ -8,6 +8,8 @@
 
 #include <stdlib.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <stdexcept>
 #include <string>
 
@@ -58,6 +60,18 @@ inline void debug_sync(cudaStream_t st, const char *what) {
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) throw Error(3, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// NVTX range on the calling host thread (every C-ABI call, every level of a
+// solve, the B products / CG / evaluation chunks): profilers attribute the
+// kernels launched inside it (ncu --nvtx --nvtx-include "msk_solve/level 2/CG/").
+// NVTX v3 is header-only; without a tool attached a push/pop is a no-op call.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    explicit NvtxRange(const std::string &name) { nvtxRangePushA(name.c_str()); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 constexpr int kMaxLevels = 16;
 
