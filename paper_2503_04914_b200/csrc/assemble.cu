@@ -4,6 +4,7 @@
 // the definition; candidates are screened by the conservative FP32 prefilter
 // first (for_each_hit, neighbors.cuh), which never drops a true neighbour.  Values Phi_delta(r) = delta^-d phi(r / delta)
 // (eq:kernelscaling P:67) with the column level's delta (reading C-1).
+#include <stdlib.h>
 #include <string.h>
 
 #include "kernels.cuh"
@@ -33,6 +34,37 @@ __global__ void __launch_bounds__(NT) k_count(LevelView rows, LevelView cols, in
     }
     if (min_r2_bits) {
         // block min of non-negative doubles via their ordered bit patterns
+        unsigned long long bits = (unsigned long long)__double_as_longlong(best);
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long t = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = t < bits ? t : bits;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMin(min_r2_bits, bits);
+    }
+}
+
+// The same counts for a whole level against itself (same, no row slice), each
+// pair visited once: row i tests only the candidates j > i, and a hit adds to
+// both rows (integer atomics: exact, order-free); the diagonal counts for i.
+// Half the candidate tests of k_count.  cnt must be zero on entry.
+template <int D>
+__global__ void __launch_bounds__(NT) k_count_sym(LevelView v, int32_t *__restrict__ cnt,
+                                                  unsigned long long *__restrict__ min_r2_bits) {
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    if (i < v.n) {
+        double x[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = v.x[a][i];
+        int c = 1;  // (i, i)
+        for_each_hit<D, 32, true>(v, x, [&](int j, double r2) {
+            ++c;
+            atomicAdd(&cnt[j], 1);
+            if (r2 < best) best = r2;
+        }, (int)i + 1);
+        atomicAdd(&cnt[i], c);
+    }
+    if (min_r2_bits) {
         unsigned long long bits = (unsigned long long)__double_as_longlong(best);
         for (int o = 16; o > 0; o >>= 1) {
             unsigned long long t = __shfl_xor_sync(0xffffffffu, bits, o);
@@ -131,6 +163,15 @@ void count_pattern(int d, const LevelView &rows, const LevelView &cols, bool sam
                    unsigned long long *min_r2_bits, cudaStream_t st, int *launches, int64_t row0) {
     if (rows.n == 0) return;
     unsigned nb = ceil_div_u(rows.n, NT);
+    static const bool sym = getenv("MSK_COUNT_SYM") == nullptr || atoi(getenv("MSK_COUNT_SYM")) != 0;
+    if (sym && same && row0 == 0 && rows.n == cols.n) {  // a whole level against itself
+        MSK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)rows.n, st));
+        if (d == 2) k_count_sym<2><<<nb, NT, 0, st>>>(rows, cnt, min_r2_bits);
+        else k_count_sym<3><<<nb, NT, 0, st>>>(rows, cnt, min_r2_bits);
+        MSK_CHECK_LAUNCH();
+        if (launches) *launches += 1;
+        return;
+    }
     if (d == 2) k_count<2><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits, row0);
     else k_count<3><<<nb, NT, 0, st>>>(rows, cols, same ? 1 : 0, cnt, min_r2_bits, row0);
     MSK_CHECK_LAUNCH();

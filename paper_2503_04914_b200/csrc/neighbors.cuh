@@ -44,8 +44,10 @@ __device__ __forceinline__ void for_each_range(const LevelView &L, const double 
 // prefilter_threshold in gather.cu: it never rejects a true neighbour), the
 // survivors are buffered (HM per thread, keeps the warp convergent) and get
 // the exact FP64 test.  Requires cols.frec (relative to cols.g.lo).
-template <int D, int HM = 32, typename F>
-__device__ __forceinline__ void for_each_hit(const LevelView &cols, const double *x, F &&f) {
+// ABOVE: only candidates j >= jmin (the ranges clipped; a symmetric count
+// visits each pair once, from its lower index).
+template <int D, int HM = 32, bool ABOVE = false, typename F>
+__device__ __forceinline__ void for_each_hit(const LevelView &cols, const double *x, F &&f, int jmin = 0) {
     float xf[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int a = 0; a < D; ++a) xf[a] = (float)(x[a] - cols.g.lo[a]);
@@ -66,6 +68,7 @@ __device__ __forceinline__ void for_each_hit(const LevelView &cols, const double
         nh = 0;
     };
     for_each_range<D>(cols, x, [&](int b, int e) {
+        if (ABOVE && b < jmin) b = jmin;
         int j = b;
         for (; j + 3 < e; j += 4) {  // four candidates per trip (independent loads)
             const float4 F0 = frec[j], F1 = frec[j + 1], F2 = frec[j + 2], F3 = frec[j + 3];

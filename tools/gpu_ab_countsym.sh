@@ -1,0 +1,8 @@
+#!/bin/bash
+# A/B of the symmetric pattern count (MSK_COUNT_SYM=0/1): C3 / C2 create phase; then the pattern tests
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
+for r in 1 2; do for c in C3 C2; do for v in 0 1; do
+  MSK_COUNT_SYM=$v timeout 600 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); p=d['config']['phase_ms']; print('$c', 'sym=$v', round(d['ms_per_step'],2), 'create', round(p['create'],3), 'assemble', round(p['assemble'],3))"
+done; done; done
+timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_large.py tests/test_gpu_fuzz.py tests/test_gpu_threshold.py tests/test_gpu_dist.py tests/test_gpu_fullsize.py -q -p no:cacheprovider 2>&1 | tail -2
