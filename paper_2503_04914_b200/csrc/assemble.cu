@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(NT) k_count_sym(LevelView v, int32_t *__restri
         int c = 1;  // (i, i)
         for_each_hit<D, 32, true>(v, x, [&](int j, double r2) {
             ++c;
+            MSK_DASSERT(j > i && j < v.n);
             atomicAdd(&cnt[j], 1);
             if (r2 < best) best = r2;
         }, (int)i + 1);

@@ -450,6 +450,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
 #pragma unroll
             for (int t = 0; t < D; ++t) y[t] = L.x[t][h];
             if (dist2_nofma<D>(xc, y) < a.rho2) {
+                MSK_DASSERT(w < np && (q + 1 == ncolz || w < ccnt[q + 1]));
                 pid[w] = h;
                 pq[w] = (uint16_t)q;
                 ++w;
@@ -507,6 +508,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
             if (!have || cc < lo) continue;
             while (m < mend && pid[m] < cc) ++m;
             if (m < mend && pid[m] == cc) {
+                MSK_DASSERT(m < np && w < prow[r] + (int)(a.row_ptr[g + 1] - a.row_ptr[g]) && w < a.nnzmax);
                 pcol[w] = (uint16_t)m;
                 pval[w] = a.val[k];
                 ++w;
@@ -522,6 +524,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         const int q = (int)((c[0] - x0) * nyb + (D == 3 ? c[1] - y0 : 0));  // the centre's own column
         for (int m = ccnt[q]; m < ccnt[q + 1]; ++m)
             if (pid[m] == (int32_t)i) ctr = m;
+        MSK_DASSERT(q >= 0 && q < ncolz && ctr >= 0);
     }
     __syncthreads();
     for (int r = tid; r < np; r += NT) {
@@ -553,6 +556,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
 #pragma unroll
                 for (int u = 0; u < 3; ++u) {
                     const int k = kk[u] + t < ke[u] ? kk[u] + t : nnz_sent;
+                    MSK_DASSERT(k <= a.nnzmax && pcol[k] < np);
                     acc[u] = fma(pval[k], Rv[pcol[k]], acc[u]);
                 }
             }
@@ -627,6 +631,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
                 for (int64_t iy = D == 3 ? cj[1] - 1 : 0; iy <= (D == 3 ? cj[1] + 1 : 0); ++iy) {
                     if (D == 3 && (iy < y0 || iy > y1)) continue;
                     const int q = (int)((ix - x0) * nyb + (iy - y0));
+                    MSK_DASSERT(q >= 0 && q < ncolz);
                     const int64_t kb = D == 3 ? (ix * L.g.dim[1] + iy) * L.g.dim[2] : ix * L.g.dim[1];
                     const int32_t b = L.cell_start[kb + zlo], e = L.cell_start[kb + zhi + 1];
                     // the members in cells zlo..zhi of this column, ascending
