@@ -792,7 +792,7 @@ void assemble_body(msk_hierarchy *h, double T, double lagrange_tol, double patch
         // MSK_COL16=1: k_cg streams 16-bit columns in per-chunk windows (10 B/nnz instead
         // of 12).  Off by default: same-box A/B C3 finest level 40.1 vs
         // 32.7 ms, C2 21.3 vs 19.4 ms -- the decode lengthens the gather's address chain,
-        // and the SpMV pass is gather-latency bound, not bandwidth bound
+        // and the SpMV pass is bound by that per-thread chain, not by bandwidth
         // The same per-chunk column windows can steer an L2 prefetch of the next chunk's
         // gathered r (MSK_RPREF=1).  Off by default: same-box A/B, C3 finest 32.91 ms
         // either way, level 5 3.46 vs 3.33 ms (the gathered r already hits L2).
