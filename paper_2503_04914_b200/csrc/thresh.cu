@@ -606,6 +606,15 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         ++it;
     }
     if (tid == 0) atomicMax(&a.fail[2], it);
+    // the members' coordinates into the CG's dead vectors (every thread left the
+    // loop after the same reduction barrier, past its last read of r, p, s):
+    // phase 4 reads them from shared memory
+    double *cx[3] = {Rv, P, S};
+    for (int r = tid; r < np; r += NT) {
+        const int32_t g = pid[r];
+#pragma unroll
+        for (int u = 0; u < D; ++u) cx[u][r] = L.x[u][g];
+    }
     __syncthreads();
     // ---- 4. values at the stored entries of column i
     const int64_t gc = a.col_off + i;
@@ -634,14 +643,23 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
                     MSK_DASSERT(q >= 0 && q < ncolz);
                     const int64_t kb = D == 3 ? (ix * L.g.dim[1] + iy) * L.g.dim[2] : ix * L.g.dim[1];
                     const int32_t b = L.cell_start[kb + zlo], e = L.cell_start[kb + zhi + 1];
-                    // the members in cells zlo..zhi of this column, ascending
-                    for (int m = ccnt[q]; m < ccnt[q + 1]; ++m) {
+                    // the members in cells zlo..zhi of this column, ascending: the first
+                    // by a binary search of the column's ids (large patches hold tens of
+                    // members per column), then up to e
+                    int m = ccnt[q], mh = ccnt[q + 1];
+                    {
+                        int hi2 = mh;
+                        while (m < hi2) {
+                            const int mid = (m + hi2) >> 1;
+                            if (pid[mid] < b) m = mid + 1; else hi2 = mid;
+                        }
+                    }
+                    for (; m < mh; ++m) {
                         const int32_t h = pid[m];
-                        if (h < b) continue;
                         if (h >= e) break;
                         double y[3];
 #pragma unroll
-                        for (int u = 0; u < D; ++u) y[u] = L.x[u][h];
+                        for (int u = 0; u < D; ++u) y[u] = cx[u][m];
                         const double r2 = dist2_nofma<D>(xj, y);
                         if (r2 < d2) s = fma(wendland<K>(sqrt(r2) * inv), X[m], s);
                     }
