@@ -609,11 +609,14 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     // the members' coordinates into the CG's dead vectors (every thread left the
     // loop after the same reduction barrier, past its last read of r, p, s):
     // phase 4 reads them from shared memory
+    // and each member's last-axis cell relative to the box into pq (dead since
+    // phase 2): a column's members are in key order, i.e. ascending in it
     double *cx[3] = {Rv, P, S};
     for (int r = tid; r < np; r += NT) {
         const int32_t g = pid[r];
 #pragma unroll
         for (int u = 0; u < D; ++u) cx[u][r] = L.x[u][g];
+        pq[r] = (uint16_t)(cell_coord(L.g, D - 1, cx[D - 1][r]) - z0);
     }
     __syncthreads();
     // ---- 4. values at the stored entries of column i
@@ -641,22 +644,19 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
                     if (D == 3 && (iy < y0 || iy > y1)) continue;
                     const int q = (int)((ix - x0) * nyb + (iy - y0));
                     MSK_DASSERT(q >= 0 && q < ncolz);
-                    const int64_t kb = D == 3 ? (ix * L.g.dim[1] + iy) * L.g.dim[2] : ix * L.g.dim[1];
-                    const int32_t b = L.cell_start[kb + zlo], e = L.cell_start[kb + zhi + 1];
                     // the members in cells zlo..zhi of this column, ascending: the first
-                    // by a binary search of the column's ids (large patches hold tens of
-                    // members per column), then up to e
+                    // by a binary search of the column's last-axis cells (large patches
+                    // hold tens of members per column), then while in the window
+                    const int zl = (int)(zlo - z0), zh = (int)(zhi - z0);
                     int m = ccnt[q], mh = ccnt[q + 1];
                     {
                         int hi2 = mh;
                         while (m < hi2) {
                             const int mid = (m + hi2) >> 1;
-                            if (pid[mid] < b) m = mid + 1; else hi2 = mid;
+                            if ((int)pq[mid] < zl) m = mid + 1; else hi2 = mid;
                         }
                     }
-                    for (; m < mh; ++m) {
-                        const int32_t h = pid[m];
-                        if (h >= e) break;
+                    for (; m < mh && (int)pq[m] <= zh; ++m) {
                         double y[3];
 #pragma unroll
                         for (int u = 0; u < D; ++u) y[u] = cx[u][m];
