@@ -16,6 +16,8 @@
 // The Jacobi sweep then is a CSR SpMV per target level (no inner solves).
 #include <vector>
 
+#include <stdlib.h>
+
 #include "kernels.cuh"
 #include "neighbors.cuh"
 
@@ -96,6 +98,41 @@ __global__ void k_csc_fill(int64_t nrows, int64_t row0, const int64_t *__restric
         const int64_t pos = cptr[c] + atomicAdd(&cur[c], 1);
         cpos[pos] = p;
         crow[pos] = (int32_t)g;
+    }
+}
+
+// The same two passes row by row with warp-aggregated atomics: the lanes of a
+// warp hold neighbouring rows, whose t-th entries mostly fall into the same
+// coarse column (a coarse column collects thousands of entries), so one
+// atomic per distinct column and warp step replaces one per entry.
+// FILL = false: counts only.  (The order inside a column stays arbitrary, as
+// with k_csc_fill: every consumer indexes by cpos.)
+template <bool FILL>
+__global__ void k_csc_agg(int64_t nrows, int64_t row0, const int64_t *__restrict__ row_ptr,
+                          const int32_t *__restrict__ col, const int64_t *__restrict__ cptr,
+                          int32_t *__restrict__ cur, int64_t *__restrict__ cpos, int32_t *__restrict__ crow) {
+    const int64_t r = (int64_t)blockIdx.x * NT + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = row0 + r;
+    int64_t p = r < nrows ? row_ptr[g] : 0;
+    const int64_t pe = r < nrows ? row_ptr[g + 1] : 0;
+    while (__any_sync(0xffffffffu, p < pe)) {
+        const bool act = p < pe;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (act) {
+            const int32_t c = col[p];
+            const unsigned grp = __match_any_sync(am, c);
+            const int leader = __ffs(grp) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&cur[c], __popc(grp));
+            if (FILL) {
+                base = __shfl_sync(grp, base, leader);
+                const int64_t pos = cptr[c] + base + __popc(grp & ((1u << lane) - 1u));
+                cpos[pos] = p;
+                crow[pos] = (int32_t)g;
+            }
+            ++p;
+        }
     }
 }
 
@@ -780,15 +817,26 @@ void thresh_csc(int64_t nrows_total, int64_t row0, int64_t nnz, int64_t ncols, c
     int32_t *cnt = nullptr;
     MSK_CUDA(cudaMallocAsync((void **)&cnt, sizeof(int32_t) * (size_t)(ncols + 1), st));
     MSK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)(ncols + 1), st));
-    if (nnz) {
+    static const bool agg = !(getenv("MSK_CSC_AGG") && getenv("MSK_CSC_AGG")[0] == '0');
+    if (agg) {  // every entry lies in rows [row0, row0 + nrows_total)
+        if (nrows_total) {
+            k_csc_agg<false><<<ceil_div_u(nrows_total, NT), NT, 0, st>>>(nrows_total, row0, row_ptr, col, cptr,
+                                                                         cnt, cpos, crow);
+            MSK_CHECK_LAUNCH();
+        }
+    } else if (nnz) {
         k_csc_count<<<ceil_div_u(nnz, NT), NT, 0, st>>>(nnz, col, cnt);
         MSK_CHECK_LAUNCH();
     }
     exclusive_scan_i64(cnt, ncols, cptr, st, launches);
     MSK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)(ncols + 1), st));
     if (nrows_total) {
-        k_csc_fill<<<ceil_div_u(nrows_total, NT), NT, 0, st>>>(nrows_total, row0, row_ptr, col, cptr, cnt,
-                                                               cpos, crow);
+        if (agg)
+            k_csc_agg<true><<<ceil_div_u(nrows_total, NT), NT, 0, st>>>(nrows_total, row0, row_ptr, col, cptr, cnt,
+                                                                        cpos, crow);
+        else
+            k_csc_fill<<<ceil_div_u(nrows_total, NT), NT, 0, st>>>(nrows_total, row0, row_ptr, col, cptr, cnt,
+                                                                   cpos, crow);
         MSK_CHECK_LAUNCH();
     }
     if (ncols && ccol) {
