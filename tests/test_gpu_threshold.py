@@ -181,6 +181,32 @@ def test_patch_global_workspace_path(msk, ctx):
     h.close()
 
 
+@pytest.mark.parametrize("R", [16.0, 24.0])
+def test_patch_lagrange_2d_shared_path(msk, ctx, R):
+    """The 2-D local-patch build through the shared-memory workspace (patches
+    of a few hundred points; the other 2-D patch test spans the coarse levels
+    and runs from the global workspace): same geometric pattern as the exact
+    build, values within a bar that falls with R - T (nu = 4 decays roughly
+    like e^{-0.4 r / q}), and the solve follows."""
+    H = halton_hierarchy("h2", 2, [1024, 4096, 16384], 4.0)
+    f = H.f()
+    h = msk.Hierarchy(ctx, H.points, H.delta, H.q, k=H.k)
+    h.assemble(T=2.0, lagrange_tol=1e-14)
+    ref = {(k, l): h.export_factor(k, l) for k in range(1, H.L) for l in range(k)}
+    a_ref, _ = h.solve(f)
+    h.assemble(T=2.0, lagrange_tol=1e-14, patch_R=R, patch_min_n=0)
+    bar = 3.0 * np.exp(-0.4 * (R - 2.0))
+    for (k, l), (rp, col, val, _) in ref.items():
+        rp2, col2, val2, _ = h.export_factor(k, l)
+        assert np.array_equal(rp, rp2) and np.array_equal(col, col2), (k, l)
+        assert np.all(np.isfinite(val2))
+        assert np.abs(val2 - val).max() <= bar * np.abs(val).max(), (k, l, R, np.abs(val2 - val).max() / np.abs(val).max())
+    a, _ = h.solve(f)
+    for l in range(H.L):
+        assert np.linalg.norm(a[l] - a_ref[l]) <= 10 * bar * np.linalg.norm(a_ref[l]), (l, R)
+    h.close()
+
+
 # ------------------------------------------------------------------ T sweep
 @pytest.mark.parametrize("name,schedule", [("C1", "pruned"), ("halton3d", "pruned"), ("C1", "literal")])
 def test_threshold_sweep_equals_fresh_builds(msk, ctx, name, schedule):
