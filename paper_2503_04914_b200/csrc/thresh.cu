@@ -26,6 +26,12 @@ namespace msk {
 namespace {
 constexpr int NT = 256;
 constexpr int NWM = NT / 32;
+#ifndef MSK_PATCH_EC
+#define MSK_PATCH_EC 6  // CSR entries per row kept in registers by the patch CG
+#endif
+#ifndef MSK_PATCH_REGC
+#define MSK_PATCH_REGC 1
+#endif
 
 template <int D>
 __global__ void __launch_bounds__(NT) k_tcount(ThreshPatternArgs a) {
@@ -573,12 +579,57 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     double rr_prev = 1.0, alpha = 0.0;
     int it = 0;
     __syncthreads();
+    // patches of at most 3 NT points (CTA-uniform): the first EC entries of each
+    // of the thread's three rows live in registers for the whole CG, so an
+    // entry costs one shared-memory load (the gathered r) instead of three
+    constexpr int EC = MSK_PATCH_EC;
+    const bool regc = MSK_PATCH_REGC && np <= 3 * NT;
+    double ev[3][EC];
+    int ecl[3][EC], nrow[3], kb3[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        const int r = tid + u * NT;
+        nrow[u] = regc && r < np ? pcnt[r] : 0;
+        kb3[u] = regc && r < np ? prow[r] : 0;
+#pragma unroll
+        for (int t = 0; t < EC; ++t) {
+            const bool in = t < nrow[u];
+            ev[u][t] = in ? pval[kb3[u] + t] : 0.0;
+            ecl[u][t] = in ? (int)pcol[kb3[u] + t] : 0;
+        }
+    }
     for (;;) {
         double vrr = 0.0, vrw = 0.0;
+        if (regc) {
+            double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int t = 0; t < EC; ++t)
+#pragma unroll
+                for (int u = 0; u < 3; ++u)
+                    if (t < nrow[u]) acc[u] = fma(ev[u][t], Rv[ecl[u][t]], acc[u]);
+            const int n = max(nrow[0], max(nrow[1], nrow[2]));
+            for (int t = EC; t < n; ++t)
+#pragma unroll
+                for (int u = 0; u < 3; ++u)
+                    if (t < nrow[u]) {
+                        const int k = kb3[u] + t;
+                        acc[u] = fma(pval[k], Rv[pcol[k]], acc[u]);
+                    }
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int r = tid + u * NT;
+                if (r < np) {
+                    W[r] = acc[u];
+                    const double rv = Rv[r];
+                    vrr += rv * rv;
+                    vrw += rv * acc[u];
+                }
+            }
+        }
         // a thread's rows rb, rb + NT, rb + 2 NT as three independent chains
         // (the loads of all three in flight; each row still sums in ascending
         // k); a finished row reads the zero sentinel entry at nnzmax
-        for (int rb = tid; rb < np; rb += 3 * NT) {
+        for (int rb = tid; !regc && rb < np; rb += 3 * NT) {
             int kk[3], ke[3];
             double acc[3] = {0.0, 0.0, 0.0};
             int n = 0;
