@@ -531,6 +531,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         int w = prow[r];
         int s = -1, m = 0, mend = 0;
         int32_t lo = 0, hi = 0;  // the current column's id range
+        bool fresh = true;       // no member of the current column looked at yet
         auto next = [&]() {
             while (++s < NS) {
                 const int ax = qx + s / (NS / 3) - 1, ay = D == 3 ? qy + s % 3 - 1 : 0;
@@ -540,6 +541,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
                 mend = ccnt[cq + 1];
                 lo = cb[cq];
                 hi = ce[cq];
+                fresh = true;
                 return true;
             }
             return false;
@@ -549,7 +551,15 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
             const int32_t cc = a.col[k];
             while (have && cc >= hi) have = next();
             if (!have || cc < lo) continue;
-            while (m < mend && pid[m] < cc) ++m;
+            if (fresh) {  // the first id of this column: binary search (tens of members per column)
+                int h2 = mend;
+                while (m < h2) {
+                    const int mid = (m + h2) >> 1;
+                    if (pid[mid] < cc) m = mid + 1; else h2 = mid;
+                }
+                fresh = false;
+            }
+            while (m < mend && pid[m] < cc) ++m;  // then a few steps per id
             if (m < mend && pid[m] == cc) {
                 MSK_DASSERT(m < np && w < prow[r] + (int)(a.row_ptr[g + 1] - a.row_ptr[g]) && w < a.nnzmax);
                 pcol[w] = (uint16_t)m;
