@@ -307,16 +307,18 @@ __global__ void __launch_bounds__(NT) k_csc_spmv_add(int64_t ncols, const int64_
 //     [ccnt[q], ccnt[q+1]) are kept, per member its column pq[];
 //  2. local CSR of A_P: row r of A_l restricted to the members.  A_l's
 //     neighbours of a point lie in the 3^(d-1) columns around its own, which
-//     are visited in ascending order with a monotone member pointer each (no
-//     search); values copied;
+//     are visited in ascending order (a binary search for the row's first id
+//     in each, then a monotone member pointer); values copied;
 //  3. CG on A_P c = e_i (x0 = 0, stop ||r|| <= lagrange_tol, reading C-9),
 //     vectors in shared memory, in the single-reduction form of k_cg (q = A r
 //     + beta q by recurrence: one fixed-order block reduction of r.r and r.Ar
-//     per iteration);
+//     per iteration); patches of <= 3 NT points keep the first MSK_PATCH_EC
+//     entries of each thread row in registers;
 //  4. for each stored entry (fine point x_j) of column i:
 //     chi~_i(x_j) = delta_l^-d sum_{h in P, r < delta_l} phi(r/delta_l) c_h,
 //     h ascending (the order of k_tvalues), visiting only the members in the
-//     3^(d-1) patch columns and z window around x_j.
+//     3^(d-1) patch columns and z window around x_j (members' coordinates
+//     and last-axis cells staged in shared memory after the CG).
 size_t patch_smem_bytes_impl(int pmax, int nnzmax, int nq) {
     size_t b = 0;
     b += sizeof(int32_t) * (size_t)pmax;          // pid
