@@ -29,6 +29,9 @@ constexpr int NWM = NT / 32;
 #ifndef MSK_PATCH_EC
 #define MSK_PATCH_EC 6  // CSR entries per row kept in registers by the patch CG
 #endif
+#ifndef MSK_MERGE_PF
+#define MSK_MERGE_PF 12  // columns per row loaded up front by the patch-local CSR merge
+#endif
 #ifndef MSK_PATCH_REGC
 #define MSK_PATCH_REGC 1
 #endif
@@ -507,9 +510,18 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     // ---- 2. local CSR of A restricted to the patch, in one pass: row r gets a
     // slot of its full A_l row length (the slots fit: the workspace is sized by
     // the largest sum of the members' row lengths), pcnt[r] of them are used
-    for (int r = tid; r < np; r += NT) {
-        const int32_t g = pid[r];
-        prow[r] = (int32_t)(a.row_ptr[g + 1] - a.row_ptr[g]);
+    for (int r0 = tid; r0 < np; r0 += 4 * NT) {  // four rows' pointer loads in flight
+        int64_t b4[4], e4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u * NT;
+            const int32_t g = r < np ? pid[r] : 0;
+            b4[u] = r < np ? a.row_ptr[g] : 0;
+            e4[u] = r < np ? a.row_ptr[g + 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (r0 + u * NT < np) prow[r0 + u * NT] = (int32_t)(e4[u] - b4[u]);
     }
     __syncthreads();
     int nslot = 0;
@@ -549,8 +561,19 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
             return false;
         };
         bool have = next();
-        for (int64_t k = a.row_ptr[g]; have && k < a.row_ptr[g + 1]; ++k) {  // ascending columns
-            const int32_t cc = a.col[k];
+        const int64_t kr0 = a.row_ptr[g], kr1 = a.row_ptr[g + 1];
+        // the row's first MSK_MERGE_PF columns loaded together (one round trip
+        // instead of one per entry), the rest as before
+        constexpr int PF = MSK_MERGE_PF;
+        int32_t cpf[PF];
+#pragma unroll
+        for (int t = 0; t < PF; ++t) cpf[t] = kr0 + t < kr1 ? a.col[kr0 + t] : 0;
+        for (int64_t k = kr0; have && k < kr1; ++k) {  // ascending columns
+            int32_t cc = 0;
+#pragma unroll
+            for (int t = 0; t < PF; ++t)
+                if (k - kr0 == t) cc = cpf[t];
+            if (k - kr0 >= PF) cc = a.col[k];
             while (have && cc >= hi) have = next();
             if (!have || cc < lo) continue;
             if (fresh) {  // the first id of this column: binary search (tens of members per column)
