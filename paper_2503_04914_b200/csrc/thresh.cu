@@ -397,10 +397,17 @@ __global__ void __launch_bounds__(NT) k_patch_count(PatchArgs a, const int32_t *
     atomicMax(pmax_out + 1, (int)(nz < 0x7fffffffll ? nz : 0x7fffffffll));
 }
 
-// exclusive block scan of cnt[0..n) in shared memory (n <= NT * k), result in place; returns the total
-__device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp /* NT */) {
+// the patch kernel's CTA size (rows per thread in the CG: RC for patches of
+// at most RC x PNT points with the register cache)
+#ifndef MSK_PNT
+#define MSK_PNT 384  // 384: C4F level-4 patches 723 -> 714 ms, levels 2/3 43/120 -> 34/112 ms (512: 828)
+#endif
+constexpr int PNT = MSK_PNT;
+constexpr int RC = PNT >= 384 ? 2 : 3;
+// exclusive block scan of cnt[0..n) in shared memory (n <= PNT * k), result in place; returns the total
+__device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp /* PNT */) {
     const int tid = threadIdx.x;
-    const int per = (n + NT - 1) / NT;
+    const int per = (n + PNT - 1) / PNT;
     int s = 0;
     for (int k = 0; k < per; ++k) {
         const int idx = tid * per + k;
@@ -410,12 +417,12 @@ __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp
     __syncthreads();
     if (tid == 0) {
         int run = 0;
-        for (int t = 0; t < NT; ++t) {
+        for (int t = 0; t < PNT; ++t) {
             const int v = tmp[t];
             tmp[t] = run;
             run += v;
         }
-        tmp[NT] = run;
+        tmp[PNT] = run;
     }
     __syncthreads();
     int run = tmp[tid];
@@ -427,7 +434,7 @@ __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp
             run += v;
         }
     }
-    const int total = tmp[NT];
+    const int total = tmp[PNT];
     __syncthreads();
     return total;
 }
@@ -436,8 +443,8 @@ __device__ __forceinline__ int block_scan_excl(int32_t *cnt, int n, int32_t *tmp
 // for patches that do not fit); every early return is CTA-uniform
 template <int D, int K>
 __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsigned char *base) {
-    __shared__ double red[2 * (NT / 32)];  // r.r and r.Ar warp partials
-    __shared__ int32_t tmp[NT + 1];
+    __shared__ double red[2 * (PNT / 32)];  // r.r and r.Ar warp partials
+    __shared__ int32_t tmp[PNT + 1];
     const int tid = threadIdx.x;
     const LevelView &L = a.Lv;
     const int pmax = a.pmax, nq = a.nq;
@@ -470,7 +477,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         if (tid == 0) atomicAdd(&a.fail[1], 1);
         return;
     }
-    for (int q = tid; q < ncolz; q += NT) {
+    for (int q = tid; q < ncolz; q += PNT) {
         int b, e, n = 0;
         patch_range<D>(L, q, x0, y0, y1, z0, z1, b, e);
         for (int h = b; h < e; ++h) {
@@ -490,7 +497,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         return;
     }
     if (tid == 0) ccnt[ncolz] = np;
-    for (int q = tid; q < ncolz; q += NT) {
+    for (int q = tid; q < ncolz; q += PNT) {
         int w = ccnt[q];
         const int b = cb[q], e = ce[q];
         for (int h = b; h < e; ++h) {
@@ -510,18 +517,18 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     // ---- 2. local CSR of A restricted to the patch, in one pass: row r gets a
     // slot of its full A_l row length (the slots fit: the workspace is sized by
     // the largest sum of the members' row lengths), pcnt[r] of them are used
-    for (int r0 = tid; r0 < np; r0 += 4 * NT) {  // four rows' pointer loads in flight
+    for (int r0 = tid; r0 < np; r0 += 4 * PNT) {  // four rows' pointer loads in flight
         int64_t b4[4], e4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int r = r0 + u * NT;
+            const int r = r0 + u * PNT;
             const int32_t g = r < np ? pid[r] : 0;
             b4[u] = r < np ? a.row_ptr[g] : 0;
             e4[u] = r < np ? a.row_ptr[g + 1] : 0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (r0 + u * NT < np) prow[r0 + u * NT] = (int32_t)(e4[u] - b4[u]);
+            if (r0 + u * PNT < np) prow[r0 + u * PNT] = (int32_t)(e4[u] - b4[u]);
     }
     __syncthreads();
     int nslot = 0;
@@ -539,7 +546,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         pcol[nnz_sent] = 0;
     }
     constexpr int NS = D == 3 ? 9 : 3;  // neighbour columns (dx, dy) in ascending key order
-    for (int r = tid; r < np; r += NT) {
+    for (int r = tid; r < np; r += PNT) {
         const int32_t g = pid[r];
         const int q = pq[r], qx = q / nyb, qy = q - qx * nyb;
         int w = prow[r];
@@ -605,7 +612,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         MSK_DASSERT(q >= 0 && q < ncolz && ctr >= 0);
     }
     __syncthreads();
-    for (int r = tid; r < np; r += NT) {
+    for (int r = tid; r < np; r += PNT) {
         X[r] = 0.0;
         Rv[r] = r == ctr ? 1.0 : 0.0;
         P[r] = 0.0;
@@ -614,16 +621,16 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     double rr_prev = 1.0, alpha = 0.0;
     int it = 0;
     __syncthreads();
-    // patches of at most 3 NT points (CTA-uniform): the first EC entries of each
+    // patches of at most 3 PNT points (CTA-uniform): the first EC entries of each
     // of the thread's three rows live in registers for the whole CG, so an
     // entry costs one shared-memory load (the gathered r) instead of three
     constexpr int EC = MSK_PATCH_EC;
-    const bool regc = MSK_PATCH_REGC && np <= 3 * NT;
-    double ev[3][EC];
-    int ecl[3][EC], nrow[3], kb3[3];
+    const bool regc = MSK_PATCH_REGC && np <= RC * PNT;
+    double ev[RC][EC];
+    int ecl[RC][EC], nrow[RC], kb3[RC];
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-        const int r = tid + u * NT;
+    for (int u = 0; u < RC; ++u) {
+        const int r = tid + u * PNT;
         nrow[u] = regc && r < np ? pcnt[r] : 0;
         kb3[u] = regc && r < np ? prow[r] : 0;
 #pragma unroll
@@ -636,23 +643,27 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     for (;;) {
         double vrr = 0.0, vrw = 0.0;
         if (regc) {
-            double acc[3] = {0.0, 0.0, 0.0};
+            double acc[RC];
+#pragma unroll
+            for (int u = 0; u < RC; ++u) acc[u] = 0.0;
 #pragma unroll
             for (int t = 0; t < EC; ++t)
 #pragma unroll
-                for (int u = 0; u < 3; ++u)
+                for (int u = 0; u < RC; ++u)
                     if (t < nrow[u]) acc[u] = fma(ev[u][t], Rv[ecl[u][t]], acc[u]);
-            const int n = max(nrow[0], max(nrow[1], nrow[2]));
+            int n = 0;
+#pragma unroll
+            for (int u = 0; u < RC; ++u) n = max(n, nrow[u]);
             for (int t = EC; t < n; ++t)
 #pragma unroll
-                for (int u = 0; u < 3; ++u)
+                for (int u = 0; u < RC; ++u)
                     if (t < nrow[u]) {
                         const int k = kb3[u] + t;
                         acc[u] = fma(pval[k], Rv[pcol[k]], acc[u]);
                     }
 #pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int r = tid + u * NT;
+            for (int u = 0; u < RC; ++u) {
+                const int r = tid + u * PNT;
                 if (r < np) {
                     W[r] = acc[u];
                     const double rv = Rv[r];
@@ -661,16 +672,16 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
                 }
             }
         }
-        // a thread's rows rb, rb + NT, rb + 2 NT as three independent chains
+        // a thread's rows rb, rb + PNT, rb + 2 PNT as three independent chains
         // (the loads of all three in flight; each row still sums in ascending
         // k); a finished row reads the zero sentinel entry at nnzmax
-        for (int rb = tid; !regc && rb < np; rb += 3 * NT) {
+        for (int rb = tid; !regc && rb < np; rb += 3 * PNT) {
             int kk[3], ke[3];
             double acc[3] = {0.0, 0.0, 0.0};
             int n = 0;
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
-                const int r = rb + u * NT;
+                const int r = rb + u * PNT;
                 kk[u] = r < np ? prow[r] : 0;
                 ke[u] = r < np ? kk[u] + pcnt[r] : 0;
                 n = max(n, ke[u] - kk[u]);
@@ -685,7 +696,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
             }
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
-                const int r = rb + u * NT;
+                const int r = rb + u * PNT;
                 if (r < np) {
                     W[r] = acc[u];
                     const double rv = Rv[r];
@@ -700,14 +711,14 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         }
         if ((tid & 31) == 0) {
             red[tid >> 5] = vrr;
-            red[NT / 32 + (tid >> 5)] = vrw;
+            red[PNT / 32 + (tid >> 5)] = vrw;
         }
         __syncthreads();
         double rr = 0.0, rw = 0.0;
 #pragma unroll
-        for (int w = 0; w < NT / 32; ++w) {  // warp order: deterministic
+        for (int w = 0; w < PNT / 32; ++w) {  // warp order: deterministic
             rr += red[w];
-            rw += red[NT / 32 + w];
+            rw += red[PNT / 32 + w];
         }
         if (rr <= a.tol2) break;
         if (it >= a.max_iter) {
@@ -717,7 +728,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
         const double beta = it == 0 ? 0.0 : rr / rr_prev;
         alpha = it == 0 ? rr / rw : rr / (rw - beta * rr / alpha);
         rr_prev = rr;
-        for (int r = tid; r < np; r += NT) {
+        for (int r = tid; r < np; r += PNT) {
             const double pn = Rv[r] + beta * P[r];
             const double sn = W[r] + beta * S[r];
             P[r] = pn;
@@ -735,7 +746,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     // and each member's last-axis cell relative to the box into pq (dead since
     // phase 2): a column's members are in key order, i.e. ascending in it
     double *cx[3] = {Rv, P, S};
-    for (int r = tid; r < np; r += NT) {
+    for (int r = tid; r < np; r += PNT) {
         const int32_t g = pid[r];
 #pragma unroll
         for (int u = 0; u < D; ++u) cx[u][r] = L.x[u][g];
@@ -747,7 +758,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
     const double d2 = L.delta2, inv = L.inv_delta;
     const int la = D - 1;
     const int64_t zf = L.g.zf;
-    for (int64_t t = a.cptr[gc] + tid; t < a.cptr[gc + 1]; t += NT) {
+    for (int64_t t = a.cptr[gc] + tid; t < a.cptr[gc + 1]; t += PNT) {
         const int64_t g = a.crow[t];
         int k = 0;
         while (k + 1 < a.L && g >= a.lev_off[k + 1]) ++k;
@@ -797,7 +808,7 @@ __device__ __forceinline__ void patch_column(const PatchArgs &a, int64_t i, unsi
 // (LDS/STS; a pointer that may be either is generic LD/ST with 64-bit
 // addresses); GWS = true: a global slice per CTA for patches that do not fit
 template <int D, int K, bool GWS>
-__global__ void __launch_bounds__(NT) k_patch(PatchArgs a, unsigned char *gws, size_t gstride) {
+__global__ void __launch_bounds__(PNT) k_patch(PatchArgs a, unsigned char *gws, size_t gstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char *base = GWS ? gws + (size_t)blockIdx.x * gstride : smem_raw;
     for (int64_t i = blockIdx.x; i < a.ncols; i += gridDim.x) {
@@ -843,9 +854,9 @@ void patch_lagrange(const PatchArgs &a, size_t smem, cudaStream_t st, int *launc
         if (!global) {                                                                           \
             MSK_CUDA(cudaFuncSetAttribute(k_patch<DD, KK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                           (int)smem));                                           \
-            k_patch<DD, KK, false><<<grid, NT, dyn, st>>>(a, gws, stride);                       \
+            k_patch<DD, KK, false><<<grid, PNT, dyn, st>>>(a, gws, stride);                       \
         } else {                                                                                 \
-            k_patch<DD, KK, true><<<grid, NT, dyn, st>>>(a, gws, stride);                        \
+            k_patch<DD, KK, true><<<grid, PNT, dyn, st>>>(a, gws, stride);                        \
         }                                                                                        \
     } while (0)
     if (a.d == 2) {
