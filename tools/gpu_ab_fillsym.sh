@@ -1,4 +1,5 @@
 #!/bin/bash
+# EXPERIMENT RECORD: the symmetric fill was removed after the measurement (profiles/r02_count_sym_ab.txt); MSK_COUNT_SYM now switches the count only
 # symmetric fill (default) vs the row-by-row fill (MSK_COUNT_SYM=0 turns both off): C3 / C2 create + assemble; then the suites
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1

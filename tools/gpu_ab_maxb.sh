@@ -1,4 +1,5 @@
 #!/bin/bash
+# EXPERIMENT RECORD: the MSK_CG_MAXB hook was removed after the measurement (profiles/r02_cg_ctas_ab.txt)
 # CTAs per CG level capped (MSK_CG_MAXB): per-level CG time on C3 levels 2-5 (microbench) and C2
 mkdir -p gpurun_out
 for cfg in C3 C2; do for lv in 2 3 4 5; do for mb in 0 74 148 296; do
